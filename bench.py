@@ -1,0 +1,337 @@
+"""GPIR server-pipeline benchmark (BASELINE.json metric: PIR queries/sec, batched).
+
+One step = one full batch through the server pipeline (ExpandQuery -> RGSW
+assembly -> RowSel -> ColTor) for B client queries against the encoded DB.
+Default workload = BASELINE configs[1]: 1 GiB encoded DB (D0=256 x D1=64
+polys, 8 KiB records at P=2^16), batch of 32 distinct clients, one B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1|2|3]
+
+`value` is device-timed QPS with queries resident in HBM; `e2e` is the same
+metric through the C ABI host entry point `gpir_answer_batch` with pinned
+host buffers (H2D of queries + D2H of responses inside the timed region).
+`--impl reference` times the CPU oracle port of the reference's answer_batch
+on this host (rank 0 only).  Multi-GPU (torchrun, one rank per GPU): each
+rank serves its own batch against its own copy of the DB shard (see
+DESIGN.md "Multi-GPU"); QPS is summed over ranks with max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(ROOT, ".numba_cache"))
+
+CONFIGS = {
+    # name: (d0, d1, B, record_bytes, plain_bits, description)
+    1: (16, 16, 1, 16384, 32, "config1: 16 MiB encoded DB (16x16, 16 KiB records, P=2^32), 1 query"),
+    2: (256, 64, 32, 8192, 16, "config2: 1 GiB encoded DB (256x64 polys, 8 KiB records, P=2^16), batch 32 clients"),
+    3: (256, 512, 128, 8192, 16, "config3: 8 GiB encoded DB (256x512 polys, 8 KiB records, P=2^16), batch 128 clients"),
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.out = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.out.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def synthetic_material(G, params, B, stages, rng):
+    """Uniform-random key and query material (all kernels are data-oblivious)."""
+    b = params.basis
+    k, n, ell = b.k, b.n, params.gadget.ell
+    qs = np.array([m.q for m in b.moduli], dtype=np.uint64)[:, None]
+
+    def uni(*shape):
+        return (rng.integers(0, 1 << 62, size=shape + (k, n), dtype=np.uint64) % qs).astype(np.uint32)
+
+    evks = uni(B, stages, ell, 2)
+    rgsw = uni(B, 2 * ell, 2)
+    queries = uni(B, 2)
+    return evks, rgsw, queries
+
+
+def cpu_reference(cfg_id, steps, warmup_cap=1):
+    """Time the CPU oracle port of answer_batch on a bounded sample: one query
+    at the workload's geometry per step.  Returns (qps, seconds, cores, sample)."""
+    import numba
+
+    from oracle import gpir_oracle as O
+
+    d0, d1, B, rb, pb, _ = CONFIGS[cfg_id]
+    cores = os.cpu_count() or 1
+    numba.set_num_threads(cores)
+    po = O.default_params(plain_bits=pb)
+    R = po.ring
+    rng = np.random.default_rng(1)
+    total = O.expansion_leaves(d0, d1, po.ell)
+    st = O.expand_stages(total)
+    uni = lambda *s: np.stack([rng.integers(0, q, size=s + (R.n,), dtype=np.uint64) for q in R.qs], axis=-2)
+    db = uni(d1, d0).reshape(d1, d0, R.k * R.n)
+    evk, rg = uni(1, st, po.ell, 2), uni(1, 2 * po.ell, 2)
+    # warm the numba transforms (JIT compile) on a tiny call
+    O.ntt(uni(2), R)
+    O.intt(uni(2), R)
+    times = []
+    for s in range(steps):
+        q = uni(1, 2)
+        t0 = time.perf_counter()
+        O.answer_batch(q, evk, rg, db, d0, d1, po)
+        times.append(time.perf_counter() - t0)
+    sec = float(np.mean(times))
+    return 1.0 / sec, sec, cores, f"1 query/step at {d0}x{d1} (P=2^{pb}) geometry, random key/query material, " \
+                                  f"numba NTT on {cores} threads, numpy elsewhere"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    d0, d1, B, rb, pb, desc = CONFIGS[args.config]
+    qps, sec, cores, sample = cpu_reference(args.config, args.steps)
+    line = {
+        "metric": "PIR queries/sec (batched)", "value": qps, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32 (mod-q int64 products)", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": desc, "d0": d0, "d1": d1, "global_batch": B, "record_bytes": rb, "plain_bits": pb},
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+
+    import torch
+
+    import paper_2604_04696_b200 as G
+    from paper_2604_04696_b200 import _native as nat
+
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    d0, d1, B, rb, pb, desc = CONFIGS[args.config]
+    params = G.HeParams(G.default_basis(4096), pb)
+    cfg = G.DbConfig(d0, d1, rb)
+    rng = np.random.default_rng(1000 + rank)
+    recs = rng.integers(0, 256, size=(cfg.records, rb), dtype=np.uint8)
+    db = G.encode_database_array(recs, cfg, params, device=dev)
+    del recs
+    ctx = db.ctx
+    lib = ctx.lib
+    total = G.planner.expansion_leaves(d0, d1, params.gadget.ell)
+    stages = G.planner.num_expand_stages(total)
+    evks, rgsw, queries = synthetic_material(G, params, B, stages, rng)
+    for b in range(B):
+        nat.check(lib.gpir_keys_put(ctx.h, b, nat.ptr(np.ascontiguousarray(evks[b])), stages,
+                                    nat.ptr(np.ascontiguousarray(rgsw[b]))), "keys")
+    slots = np.arange(B, dtype=np.int32)
+    words = queries.size
+    d_q = torch.from_numpy(queries.view(np.int32).reshape(-1)).to(f"cuda:{dev}")
+    d_o = torch.empty_like(d_q)
+    stream = torch.cuda.current_stream(dev)
+    sptr = C.c_void_p(stream.cuda_stream)
+    em = np.zeros(16, np.uint8)
+    cm = np.zeros(16, np.uint8)
+    nat.check(lib.gpir_plan(ctx.h, d0, d1, B, nat.ptr(em, C.c_uint8), 16, nat.ptr(cm, C.c_uint8), 16), "plan")
+    if args.modes:
+        em[:] = 1 if args.modes == "fused" else 0
+        cm[:] = em[0]
+    st = nat.GpirStats()
+
+    def step(stats=None):
+        nat.check(lib.gpir_answer_batch_dev(ctx.h, db.handle, C.c_void_p(d_q.data_ptr()),
+                                            nat.ptr(slots, C.c_int32), B, nat.ptr(em, C.c_uint8), 16,
+                                            nat.ptr(cm, C.c_uint8), 16, C.c_void_p(d_o.data_ptr()), sptr,
+                                            C.byref(stats) if stats is not None else None), "answer")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # phase breakdown + RowSel kernel duration, CUDA events on the launch stream (untimed pass)
+    ph = {"ExpandQuery": [], "RgswAssembly": [], "RowSel": [], "ColTor": [], "total": []}
+    launches = 0
+    for _ in range(max(1, min(args.steps, 5))):
+        step(st)
+        ph["ExpandQuery"].append(st.ms_expand)
+        ph["RgswAssembly"].append(st.ms_rgsw)
+        ph["RowSel"].append(st.ms_rowsel_kernel)
+        ph["ColTor"].append(st.ms_coltor)
+        ph["total"].append(st.ms_total)
+        launches = st.launches + 2
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    qps = world * B / (ms / 1e3)
+
+    # e2e: the C-ABI host entry point with pinned host buffers
+    h_q = torch.from_numpy(queries.view(np.int32).reshape(-1)).pin_memory()
+    h_o = torch.empty_like(h_q).pin_memory()
+
+    def e2e_step():
+        nat.check(lib.gpir_answer_batch(ctx.h, db.handle, C.cast(h_q.data_ptr(), nat._u32p),
+                                        nat.ptr(slots, C.c_int32), B, nat.ptr(em, C.c_uint8), 16,
+                                        nat.ptr(cm, C.c_uint8), 16, C.cast(h_o.data_ptr(), nat._u32p), None),
+                  "answer(host)")
+
+    for _ in range(2):
+        e2e_step()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_qps = world * B / e2e_s
+
+    if rank != 0:
+        return
+    hbm, peak_kind = _peaks()
+    KN = params.basis.k * params.basis.n
+    rs_bytes = d0 * d1 * KN * 4 + B * d0 * 2 * KN * 4 + B * d1 * 2 * KN * 4
+    rs_ms = float(np.mean(ph["RowSel"]))
+    achieved = rs_bytes / (rs_ms / 1e3) / 1e9
+    line = {
+        "metric": "PIR queries/sec (batched)", "value": qps, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32 (mod-q, 64-bit lazy products)",
+        "data": "synthetic (random records, uniform-random key/query material)",
+        "config": {"workload": desc, "d0": d0, "d1": d1, "global_batch": B * world, "per_gpu_batch": B,
+                   "record_bytes": rb, "plain_bits": pb, "encoded_db_bytes": d0 * d1 * KN * 4,
+                   "l2": "inputs larger than L2 (1 GiB DB streamed by RowSel every step)",
+                   "parallelism": "replica" if world > 1 else "single",
+                   "plan_eq": "".join("F" if v else "o" for v in em[:stages]),
+                   "plan_ct": "".join("F" if v else "o" for v in cm[:max(d1.bit_length() - 1, 0)])},
+        "phases_ms": {k: float(np.mean(v)) for k, v in ph.items()},
+        "gpu_launches": launches * args.steps,
+        "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": words * 4,
+                "d2h_bytes_per_step": words * 4},
+        "roofline": {"kernel": "k_rowsel_cc (RowSel)", "bound": "hbm", "achieved": achieved, "peak": hbm,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "algorithmic_bytes": rs_bytes, "avg_launch_ms": rs_ms},
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu:
+        cq, csec, cores, sample = cpu_reference(args.config, 1)
+        line["cpu_baseline"] = {"value": cq, "unit": "queries/s", "cores": cores, "kind": "port", "sample": sample}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--modes", default="", choices=["", "fused", "op"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        if args.impl == "ours":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        else:
+            dist.init_process_group("gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,138 @@
+/*
+ * gpir.h — C ABI of the B200-native GPIR server pipeline (libgpir.so).
+ *
+ * Drop-in boundary for the reference's server path (`latpir`, Python):
+ *   encode_database  src/protocol.py:118-153   -> gpir_db_encode / gpir_db_upload
+ *   ClientKeys upload (evk_raw / sk_rgsw_raw)
+ *                    src/protocol.py:165-199   -> gpir_keys_put
+ *   answer_batch     src/protocol.py:635-682   -> gpir_answer_batch (host buffers)
+ *                                               gpir_answer_batch_dev (device buffers)
+ *   expand_query_batch src/protocol.py:322-367 -> gpir_expand_dev
+ *   row_select_raw   src/protocol.py:448-492   -> gpir_rowsel_dev
+ *   col_tournament_batch src/protocol.py:542-573 -> gpir_coltor_dev
+ * Operator-level parity entry points (host buffers, reference natural order):
+ *   ntt_raw / intt_raw      src/ring.py:408-453     -> gpir_op_ntt
+ *   DigitExtractor          src/he.py:323-367       -> gpir_op_digits
+ *   planner.expand_stage    src/planner.py:321-381  -> gpir_op_expand_stage
+ *   planner.external_product_batch src/planner.py:384-435 -> gpir_op_ext_product
+ *   planner.coltor_stage    src/planner.py:438-463  -> gpir_op_coltor_stage
+ *   layout.gemm_* (p-major) src/layout.py:190-294   -> gpir_op_rowsel
+ *
+ * Conventions: all residues are uint32 canonical (< q_i < 2^31); every
+ * ciphertext is [2][k][n] (a then b), every polynomial [k][n], NTT-domain
+ * values in the reference's NATURAL slot order at this boundary.  Functions
+ * return 0 on success, a negative gpir_status otherwise; gpir_last_error()
+ * gives the message (thread-local).  Contexts are thread-safe (one internal
+ * mutex per context).  Stage modes: 0 = operation-level, 1 = stage-fused
+ * (planner.ExecMode OPERATION_LEVEL / STAGE_LEVEL, src/planner.py:105-107).
+ */
+#ifndef GPIR_H
+#define GPIR_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gpir_ctx gpir_ctx;
+typedef struct gpir_db gpir_db;
+
+enum gpir_status {
+  GPIR_OK = 0,
+  GPIR_INVALID_ARGUMENT = -1, /* latpir.errors.InvalidArgument */
+  GPIR_INVALID_STATE = -2,    /* latpir.errors.InvalidState    */
+  GPIR_INVALID_CONFIG = -3,   /* latpir.errors.InvalidConfig   */
+  GPIR_CUDA_ERROR = -4,
+  GPIR_UNSUPPORTED = -5
+};
+
+typedef struct gpir_stats {
+  float ms_expand;   /* ExpandQuery                     */
+  float ms_rgsw;     /* RGSW assembly                   */
+  float ms_rowsel;   /* RowSel                          */
+  float ms_coltor;   /* ColTor                          */
+  float ms_total;    /* device time of the whole batch  */
+  float ms_h2d;      /* host->device of queries (host API only) */
+  float ms_d2h;      /* device->host of responses (host API only) */
+  uint32_t launches; /* kernels launched for the batch  */
+  float ms_rowsel_kernel; /* RowSel GEMM kernel alone      */
+} gpir_stats;
+
+const char* gpir_last_error(void);
+const char* gpir_version(void);
+
+/* Context: ring degree n (power of two), k primes q[i] with 2n-th roots psi[i]
+ * (src/ring.py:122-158), gadget z = 2^z_bits with ell digits (src/he.py:45-55). */
+gpir_ctx* gpir_ctx_create(int device, uint32_t n, uint32_t k, const uint32_t* q, const uint32_t* psi,
+                          uint32_t z_bits, uint32_t ell);
+void gpir_ctx_destroy(gpir_ctx* ctx);
+int gpir_ctx_device(const gpir_ctx* ctx);
+/* Supported (log2 n, k, ell) combinations are compiled in; 1 if supported. */
+int gpir_supported(uint32_t n, uint32_t k, uint32_t ell);
+
+/* Database: d0 x d1 grid of records, row-major flat index r = i*d1 + j
+ * (src/protocol.py:58-61).  encode: raw bytes, record_bytes each, packed as
+ * little-endian plain_bits/8-byte words, centered mod P, lifted and NTT'd on
+ * the GPU (src/protocol.py:102-153).  upload: an already-encoded P-major
+ * (d1, d0, k*n) tensor in natural order (EncodedDatabase.data). */
+gpir_db* gpir_db_encode(gpir_ctx* ctx, const uint8_t* records, uint32_t d0, uint32_t d1, uint32_t record_bytes,
+                        uint32_t plain_bits);
+gpir_db* gpir_db_upload(gpir_ctx* ctx, const uint32_t* pmajor, uint32_t d0, uint32_t d1);
+/* Download the encoded DB back as the reference's P-major natural tensor. */
+int gpir_db_download(gpir_ctx* ctx, const gpir_db* db, uint32_t* pmajor_out);
+void gpir_db_destroy(gpir_ctx* ctx, gpir_db* db);
+size_t gpir_db_bytes(const gpir_db* db);
+
+/* Client key material, stored in key slot `slot`: evks[stages][ell][2][k][n]
+ * (stage t uses k_aut = n/2^t + 1, src/he.py:225-241) and sk_rgsw[2 ell][2][k][n]
+ * (may be NULL when the DB has one column). */
+int gpir_keys_put(gpir_ctx* ctx, int slot, const uint32_t* evks, uint32_t stages, const uint32_t* sk_rgsw);
+int gpir_keys_drop(gpir_ctx* ctx, int slot);
+
+/* Full server pipeline for B queries (src/protocol.py:635-682).
+ * queries[B][2][k][n] host; key_slots[B]; modes: one byte per ExpandQuery stage
+ * (n_eq) and per ColTor stage (n_ct), or NULL for the built-in B200 plan;
+ * responses_out[B][2][k][n] host.  stats may be NULL. */
+int gpir_answer_batch(gpir_ctx* ctx, const gpir_db* db, const uint32_t* queries, const int32_t* key_slots,
+                      uint32_t B, const uint8_t* eq_modes, uint32_t n_eq, const uint8_t* ct_modes, uint32_t n_ct,
+                      uint32_t* responses_out, gpir_stats* stats);
+/* Same with device pointers (natural order in/out) on `stream` (cudaStream_t or NULL). */
+int gpir_answer_batch_dev(gpir_ctx* ctx, const gpir_db* db, const uint32_t* d_queries, const int32_t* key_slots,
+                          uint32_t B, const uint8_t* eq_modes, uint32_t n_eq, const uint8_t* ct_modes, uint32_t n_ct,
+                          uint32_t* d_responses, void* stream, gpir_stats* stats);
+
+/* Built-in B200 hybrid plan (per-stage op/fused choice) for a geometry/batch. */
+int gpir_plan(gpir_ctx* ctx, uint32_t d0, uint32_t d1, uint32_t B, uint8_t* eq_modes, uint32_t n_eq,
+              uint8_t* ct_modes, uint32_t n_ct);
+
+/* ---- sharded pipeline pieces (multi-GPU, D1 column shards; src/cluster.py:252-265) ----
+ * gpir_shard_answer: expansion over the FULL geometry (d0, d1_total), RowSel +
+ * the low log2(d1_shard) ColTor stages on the local column shard (db holds
+ * d1_shard columns), writes one partial ct per query (natural order) to
+ * d_partials[B][2][k][n] and the high-bit RGSWs (natural order) to
+ * d_high_rgsw[B][log2(d1_total/d1_shard)][2 ell][2][k][n] (may be NULL). */
+int gpir_shard_answer(gpir_ctx* ctx, const gpir_db* db, uint32_t d1_total, const uint32_t* d_queries,
+                      const int32_t* key_slots, uint32_t B, uint32_t* d_partials, uint32_t* d_high_rgsw,
+                      void* stream, gpir_stats* stats);
+/* Residual tournament: d_cts[B][C][2][k][n] (C power of two) with
+ * d_rgsw[B][log2 C][2 ell][2][k][n], natural order -> d_out[B][2][k][n]. */
+int gpir_coltor_dev(gpir_ctx* ctx, const uint32_t* d_cts, uint32_t B, uint32_t C, const uint32_t* d_rgsw,
+                    uint32_t* d_out, void* stream);
+
+/* ---- operator-level parity entry points (host buffers, natural order) ---- */
+int gpir_op_ntt(gpir_ctx* ctx, const uint32_t* in, uint32_t* out, uint32_t polys, int inverse);
+int gpir_op_digits(gpir_ctx* ctx, const uint32_t* coeff, int32_t* digits_out, uint32_t polys);
+int gpir_op_expand_stage(gpir_ctx* ctx, const uint32_t* state, uint32_t B, uint32_t C, const uint32_t* ksk,
+                         uint32_t stage, int mode, uint32_t* out /* [B][2C] */);
+int gpir_op_ext_product(gpir_ctx* ctx, const uint32_t* cts, uint32_t B, uint32_t M, const uint32_t* rows,
+                        int mode, uint32_t* out);
+int gpir_op_coltor_stage(gpir_ctx* ctx, const uint32_t* state, uint32_t B, uint32_t C, const uint32_t* rows,
+                         int mode, uint32_t* out /* [B][C/2] */);
+int gpir_op_rowsel(gpir_ctx* ctx, const uint32_t* row_cts /* [B][d0][2][k][n] */, uint32_t B, const gpir_db* db,
+                   uint32_t* selected /* [B][d1][2][k][n] */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPIR_H */

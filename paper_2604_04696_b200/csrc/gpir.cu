@@ -1,0 +1,1139 @@
+// libgpir: host engine + C ABI (include/gpir.h) for the GPIR server pipeline
+// on B200 (sm_100a).  One context per device; all device memory is owned by
+// the context (keys, DB, pooled per-batch workspace); work is issued on one
+// stream per call and timed with CUDA events per phase.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/gpir.h"
+#include "kernels.cuh"
+
+using namespace gpir;
+
+static thread_local std::string g_err;
+
+#define FAIL(code, msg)  \
+  do {                   \
+    g_err = (msg);       \
+    return (code);       \
+  } while (0)
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      g_err = std::string(#call) + ": " + cudaGetErrorString(e_);                       \
+      return GPIR_CUDA_ERROR;                                                           \
+    }                                                                                   \
+  } while (0)
+
+#define CKL()                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess) {                                                             \
+      g_err = std::string("kernel launch: ") + cudaGetErrorString(e_);                   \
+      return GPIR_CUDA_ERROR;                                                            \
+    }                                                                                    \
+  } while (0)
+
+typedef unsigned __int128 u128;
+
+// ---------------------------------------------------------------------------
+// device buffer helper
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want) {
+    if (want <= bytes) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (want == 0) return 0;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      g_err = std::string("cudaMalloc(") + std::to_string(want) + "): " + cudaGetErrorString(e);
+      p = nullptr;
+      return GPIR_CUDA_ERROR;
+    }
+    bytes = want;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+struct gpir_db {
+  uint32_t d0 = 0, d1 = 0;
+  DevBuf data;  // (d1, d0, k, n) brv
+};
+
+struct gpir_ctx {
+  int device = 0;
+  uint32_t n = 0, logn = 0, k = 0, ell = 0, z_bits = 0;
+  std::vector<uint32_t> q, psi;
+  Tables tb{};
+  CrtConst cc{};
+  DevBuf tw_fwd, tw_inv, mono;
+  // key pool
+  uint32_t key_slots = 0, key_stages = 0;
+  std::vector<int> slot_stages;  // -1 = empty
+  std::vector<char> slot_rgsw;
+  DevBuf evk_pool, rgsw_pool;
+  // workspace
+  DevBuf ws_state0, ws_state1, ws_arows, ws_sel, ws_ct0, ws_ct1, ws_kslot;
+  DevBuf ws_coeff, ws_dig, ws_dn, ws_io0, ws_io1;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[12];
+  std::mutex mu;
+  size_t ct_words() const { return 2 * (size_t)k * n; }
+};
+
+// ---------------------------------------------------------------------------
+// host-side math for tables
+
+static uint64_t powmod(uint64_t b, uint64_t e, uint64_t m) {
+  uint64_t r = 1 % m;
+  b %= m;
+  while (e) {
+    if (e & 1) r = (u128)r * b % m;
+    b = (u128)b * b % m;
+    e >>= 1;
+  }
+  return r;
+}
+static uint32_t shoup(uint32_t w, uint32_t q) { return (uint32_t)(((uint64_t)w << 32) / q); }
+static uint32_t hbrv(uint32_t x, int logn) {
+  uint32_t r = 0;
+  for (int b = 0; b < logn; ++b) r |= ((x >> b) & 1u) << (logn - 1 - b);
+  return r;
+}
+
+static int build_tables(gpir_ctx* c) {
+  const uint32_t n = c->n, k = c->k;
+  std::vector<uint2> fwd((size_t)k * n), inv((size_t)k * n), mono((size_t)c->logn * k * n);
+  for (uint32_t i = 0; i < k; ++i) {
+    const uint32_t q = c->q[i];
+    const uint64_t psi = c->psi[i];
+    const uint64_t ipsi = powmod(psi, q - 2, q);
+    std::vector<uint32_t> pw(2 * n), ipw(2 * n);
+    uint64_t v = 1, iv = 1;
+    for (uint32_t e = 0; e < 2 * n; ++e) {
+      pw[e] = (uint32_t)v;
+      ipw[e] = (uint32_t)iv;
+      v = v * psi % q;
+      iv = iv * ipsi % q;
+    }
+    for (uint32_t m = 0; m < n; ++m) {
+      const uint32_t w = pw[hbrv(m, c->logn)], iw = ipw[hbrv(m, c->logn)];
+      fwd[(size_t)i * n + m] = make_uint2(w, shoup(w, q));
+      inv[(size_t)i * n + m] = make_uint2(iw, shoup(iw, q));
+    }
+    // X^{-2^t} in brv layout: slot s holds psi^((2 brv(s) + 1) e), e = -2^t mod 2n  (src/ring.py:667-673)
+    for (uint32_t t = 0; t < c->logn; ++t) {
+      const uint64_t e = (2ull * n - (1ull << t)) % (2ull * n);
+      for (uint32_t s = 0; s < n; ++s) {
+        const uint64_t ex = ((2ull * hbrv(s, c->logn) + 1) * e) % (2ull * n);
+        const uint32_t w = pw[ex];
+        mono[((size_t)t * k + i) * n + s] = make_uint2(w, shoup(w, q));
+      }
+    }
+    Modulus& M = c->tb.mod[i];
+    M.q = q;
+    uint32_t inv32 = 1;  // q^{-1} mod 2^32 by Newton
+    for (int it = 0; it < 5; ++it) inv32 *= 2 - q * inv32;
+    M.qinv_neg = (uint32_t)(0u - inv32);
+    M.r2 = (uint32_t)((((u128)1) << 64) % q);
+    M.barrett = (uint32_t)((1ull << 32) / q);
+    M.ninv = (uint32_t)powmod(n, q - 2, q);
+    M.ninv_sh = shoup(M.ninv, q);
+  }
+  // CRT constants (src/ring.py:214-235)
+  u128 Q = 1;
+  for (uint32_t i = 0; i < k; ++i) Q *= c->q[i];
+  CrtConst& cc = c->cc;
+  cc.k = (int)k;
+  cc.ell = (int)c->ell;
+  cc.z_bits = (int)c->z_bits;
+  cc.logn = (int)c->logn;
+  for (uint32_t i = 0; i < k; ++i) {
+    const u128 m = Q / c->q[i];
+    cc.m_lo[i] = (uint64_t)m;
+    cc.m_hi[i] = (uint64_t)(m >> 64);
+    const uint32_t mh = (uint32_t)powmod((uint64_t)(m % c->q[i]), c->q[i] - 2, c->q[i]);
+    c->tb.mod[i].mhat = mh;
+    c->tb.mod[i].mhat_sh = shoup(mh, c->q[i]);
+  }
+  cc.q_lo = (uint64_t)Q;
+  cc.q_hi = (uint64_t)(Q >> 64);
+  const u128 half = (Q - 1) / 2;
+  cc.half_lo = (uint64_t)half;
+  cc.half_hi = (uint64_t)(half >> 64);
+  uint32_t t = 1;
+  while (t < k) t *= 2;
+  cc.n_red = 0;
+  while (t >= 1) {
+    const u128 r = Q * t;
+    cc.red_lo[cc.n_red] = (uint64_t)r;
+    cc.red_hi[cc.n_red] = (uint64_t)(r >> 64);
+    ++cc.n_red;
+    t /= 2;
+  }
+  int rc;
+  if ((rc = c->tw_fwd.ensure(fwd.size() * sizeof(uint2)))) return rc;
+  if ((rc = c->tw_inv.ensure(inv.size() * sizeof(uint2)))) return rc;
+  if ((rc = c->mono.ensure(mono.size() * sizeof(uint2)))) return rc;
+  CK(cudaMemcpy(c->tw_fwd.p, fwd.data(), fwd.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->tw_inv.p, inv.data(), inv.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->mono.p, mono.data(), mono.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+  c->tb.fwd = c->tw_fwd.as<uint2>();
+  c->tb.inv = c->tw_inv.as<uint2>();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// geometry (src/planner.py:153-173)
+
+static uint32_t ilog2(uint32_t v) {
+  uint32_t r = 0;
+  while ((1u << r) < v) ++r;
+  return r;
+}
+static uint32_t leaves_of(uint32_t d0, uint32_t d1, uint32_t ell) { return d0 + ilog2(d1) * ell; }
+static uint32_t stages_of(uint32_t total) { return total > 1 ? ilog2(total) : 0; }
+
+// ---------------------------------------------------------------------------
+// templated engine
+
+static int bitrev_rows(gpir_ctx* c, const uint32_t* in, uint32_t* out, size_t rows, cudaStream_t s) {
+  const size_t tot = rows << c->logn;
+  if (!tot) return 0;
+  k_bitrev_rows<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(in, out, rows, (int)c->logn);
+  CKL();
+  return 0;
+}
+
+template <int LOGN, int K, int ELL>
+struct Engine {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int T = NttCfg<LOGN>::T;
+  static constexpr size_t CT = 2 * (size_t)K * N;
+  static size_t fused_smem() { return (size_t)N * 4 + (size_t)priv_slots<K, ELL>() * 16 * T * 4; }
+
+  static int setup_attrs() {
+    static bool done = false;
+    if (done) return 0;
+    const int sm = (int)fused_smem();
+    CK(cudaFuncSetAttribute(k_eq_fused<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute(k_xp_fused<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    done = true;
+    return 0;
+  }
+
+  // op-level scratch sizing: nodes per chunk bounded by ~1 GiB
+  static size_t op_chunk(size_t per_node_words) {
+    const size_t budget = (size_t)1 << 28;  // words (1 GiB)
+    return std::max<size_t>(1, budget / per_node_words);
+  }
+
+  // one ExpandQuery stage: state (B, C) -> out (B, Cout)
+  static int expand_stage(gpir_ctx* c, const u32* state, int B, int C, u32* out, int Cout, int t, RowsDesc ksk,
+                          int mode, cudaStream_t s, uint32_t* launches) {
+    const u32 k_aut = (u32)(N >> t) + 1;
+    const uint2* mono = c->mono.as<uint2>() + (size_t)t * K * N;
+    int rc;
+    if (mode == 1) {
+      if ((rc = setup_attrs())) return rc;
+      k_eq_fused<LOGN, K, ELL><<<B * C, T, fused_smem(), s>>>(state, C, out, Cout, ksk, k_aut, mono, c->tb, c->cc);
+      CKL();
+      ++*launches;
+      return 0;
+    }
+    const size_t per = (size_t)K * N + (size_t)ELL * N + (size_t)ELL * K * N;
+    const size_t chunk = op_chunk(per);
+    const size_t nodes = (size_t)B * C;
+    const size_t cn = std::min(chunk, nodes);
+    if ((rc = c->ws_coeff.ensure(cn * K * N * 4))) return rc;
+    if ((rc = c->ws_dig.ensure(cn * ELL * N * 4))) return rc;
+    if ((rc = c->ws_dn.ensure(cn * ELL * K * N * 4))) return rc;
+    for (size_t n0 = 0; n0 < nodes; n0 += cn) {
+      const int nn = (int)std::min(cn, nodes - n0);
+      k_op_eq_intt<LOGN, K><<<dim3(nn, K), T, 0, s>>>(state, (int)n0, k_aut, c->ws_coeff.as<u32>(), c->tb);
+      CKL();
+      const size_t tot = (size_t)nn * N;
+      k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), nn,
+                                                                          c->ws_dig.as<int>(), c->tb, c->cc);
+      CKL();
+      k_op_digit_ntt<LOGN, K><<<dim3(nn * ELL, K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(), c->tb);
+      CKL();
+      const size_t tm = (size_t)nn * K * N;
+      k_op_eq_mac<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(
+          state, C, (int)n0, nn, c->ws_dn.as<u32>(), ksk, k_aut, mono, out, Cout, c->tb);
+      CKL();
+      *launches += 4;
+    }
+    return 0;
+  }
+
+  // batched external products: (B, M) cts (or ColTor pairs) -> out (B, M)
+  static int ext_product(gpir_ctx* c, const u32* in, size_t in_b, int B, int M, int pairs, u32* out, size_t out_b,
+                         RowsDesc rows, int mode, cudaStream_t s, uint32_t* launches) {
+    int rc;
+    if (B * M == 0) return 0;
+    if (mode == 1) {
+      if ((rc = setup_attrs())) return rc;
+      k_xp_fused<LOGN, K, ELL><<<B * M, T, fused_smem(), s>>>(in, in_b, M, pairs, out, out_b, rows, c->tb, c->cc);
+      CKL();
+      ++*launches;
+      return 0;
+    }
+    const size_t per = 2 * ((size_t)K * N + (size_t)ELL * N + (size_t)ELL * K * N);
+    const size_t chunk = op_chunk(per);
+    const size_t cts = (size_t)B * M;
+    const size_t cn = std::min(chunk, cts);
+    if ((rc = c->ws_coeff.ensure(cn * 2 * K * N * 4))) return rc;
+    if ((rc = c->ws_dig.ensure(cn * 2 * ELL * N * 4))) return rc;
+    if ((rc = c->ws_dn.ensure(cn * 2 * ELL * K * N * 4))) return rc;
+    for (size_t m0 = 0; m0 < cts; m0 += cn) {
+      const int nn = (int)std::min(cn, cts - m0);
+      k_op_xp_intt<LOGN, K><<<dim3(2 * nn, K), T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_coeff.as<u32>(), c->tb);
+      CKL();
+      const size_t tot = (size_t)2 * nn * N;
+      k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), 2 * nn,
+                                                                          c->ws_dig.as<int>(), c->tb, c->cc);
+      CKL();
+      k_op_digit_ntt<LOGN, K><<<dim3(2 * nn * ELL, K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(), c->tb);
+      CKL();
+      const size_t tm = (size_t)nn * K * N;
+      k_op_xp_mac<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(in, in_b, M, (int)m0, nn, pairs,
+                                                                             c->ws_dn.as<u32>(), rows, out, out_b,
+                                                                             c->tb);
+      CKL();
+      *launches += 4;
+    }
+    return 0;
+  }
+
+  static int rowsel(gpir_ctx* c, const u32* leaves, size_t a_b_words, int B, const gpir_db* db, u32* sel,
+                    cudaStream_t s, uint32_t* launches) {
+    const int KN = K * N;
+    const int mt = (2 * B + RS_MT - 1) / RS_MT, nt = ((int)db->d1 + RS_NT - 1) / RS_NT;
+    dim3 grid(mt * nt, KN / 32);
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_rowsel_cc, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_SMEM));
+      attr = true;
+    }
+    k_rowsel_cc<<<grid, 256, RS_SMEM, s>>>(leaves, a_b_words, 2 * B, db->data.as<u32>(), (int)db->d0, (int)db->d1, sel, KN,
+                                     LOGN, c->tb);
+    CKL();
+    ++*launches;
+    return 0;
+  }
+
+  static RowsDesc evk_rows(gpir_ctx* c, int t, const int* kslot) {
+    RowsDesc r;
+    r.lo = c->evk_pool.as<u32>() + (size_t)t * ELL * CT;
+    r.lo_b = (size_t)c->key_stages * ELL * CT;
+    r.hi = r.lo;
+    r.hi_b = r.lo_b;
+    r.slot = kslot;
+    return r;
+  }
+  static RowsDesc skrgsw_rows(gpir_ctx* c, const int* kslot) {
+    RowsDesc r;
+    r.lo = c->rgsw_pool.as<u32>();
+    r.lo_b = 2 * (size_t)ELL * CT;
+    r.hi = r.lo + (size_t)ELL * CT;
+    r.hi_b = r.lo_b;
+    r.slot = kslot;
+    return r;
+  }
+
+  // expansion of B brv queries (in ws_state0 as (B,1)) -> leaves pointer (B, total)
+  static int expand_all(gpir_ctx* c, int B, uint32_t total, const uint8_t* eq_modes, uint32_t n_eq,
+                        const int* kslot, u32** leaves_out, cudaStream_t s, uint32_t* launches) {
+    const uint32_t stages = stages_of(total);
+    u32* cur = c->ws_state0.as<u32>();
+    u32* nxt = c->ws_state1.as<u32>();
+    for (uint32_t t = 0; t < stages; ++t) {
+      const int C = (int)std::min<uint32_t>(1u << t, total);
+      const int Cout = (int)std::min<uint32_t>(2u << t, total);
+      const int mode = (eq_modes && t < n_eq) ? eq_modes[t] : default_mode(B * C);
+      int rc = expand_stage(c, cur, B, C, nxt, Cout, (int)t, evk_rows(c, (int)t, kslot), mode, s, launches);
+      if (rc) return rc;
+      std::swap(cur, nxt);
+    }
+    *leaves_out = cur;
+    return 0;
+  }
+
+  static int default_mode(size_t nodes) {
+    // B200 hybrid rule: the fused kernel runs one CTA (T threads, ~96 KiB smem) per
+    // node; below ~2 waves of 148 SMs x 2 CTAs the operation-level kernels (which
+    // expose ELL*K-fold more CTAs) win.
+    return nodes >= 2 * 148 * 2 ? 1 : 0;
+  }
+
+  static int ensure_ws(gpir_ctx* c, int B, uint32_t total, uint32_t d1, uint32_t bits) {
+    int rc;
+    const size_t ctb = CT * 4;
+    if ((rc = c->ws_state0.ensure((size_t)B * total * ctb))) return rc;
+    if ((rc = c->ws_state1.ensure((size_t)B * total * ctb))) return rc;
+    if ((rc = c->ws_arows.ensure((size_t)B * std::max<uint32_t>(bits, 1) * ELL * ctb))) return rc;
+    if ((rc = c->ws_sel.ensure((size_t)B * d1 * ctb))) return rc;
+    if ((rc = c->ws_ct0.ensure((size_t)B * std::max<uint32_t>(d1 / 2, 1) * ctb))) return rc;
+    if ((rc = c->ws_ct1.ensure((size_t)B * std::max<uint32_t>(d1 / 4, 1) * ctb))) return rc;
+    if ((rc = c->ws_kslot.ensure((size_t)B * 4))) return rc;
+    return 0;
+  }
+
+  // Full pipeline on device, brv queries already in ws_state0 as (B, 1).
+  // Runs expansion over (d0, d1_tree), RGSW assembly for all log2(d1_tree)
+  // bits, RowSel on db, and the low log2(db->d1) ColTor stages; returns the
+  // pointer to the (B, 1) brv result and the leaves / a-rows for the caller.
+  static int pipeline(gpir_ctx* c, const gpir_db* db, uint32_t d1_tree, int B, const uint8_t* eq_modes, uint32_t n_eq,
+                      const uint8_t* ct_modes, uint32_t n_ct, const int* kslot, cudaStream_t s, gpir_stats* st,
+                      u32** result, u32** leaves_out) {
+    const uint32_t d0 = db->d0, d1 = db->d1;
+    const uint32_t total = leaves_of(d0, d1_tree, ELL);
+    const uint32_t bits_tree = ilog2(d1_tree), bits = ilog2(d1);
+    uint32_t launches = 0;
+    int rc;
+    if (st) CK(cudaEventRecord(c->ev[1], s));
+    u32* leaves = nullptr;
+    if ((rc = expand_all(c, B, total, eq_modes, n_eq, kslot, &leaves, s, &launches))) return rc;
+    if (st) CK(cudaEventRecord(c->ev[2], s));
+    // RGSW assembly (src/protocol.py:383-409): a-rows = col_cts ⊡ RGSW(s)
+    if (bits_tree > 0) {
+      const int M = (int)(bits_tree * ELL);
+      const int mode = default_mode((size_t)B * M);
+      if ((rc = ext_product(c, leaves + (size_t)d0 * CT, total, B, M, 0, c->ws_arows.as<u32>(), (size_t)M,
+                            skrgsw_rows(c, kslot), mode, s, &launches)))
+        return rc;
+    }
+    if (st) CK(cudaEventRecord(c->ev[3], s));
+    if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches))) return rc;
+    if (st) CK(cudaEventRecord(c->ev[4], s));
+    // ColTor (src/protocol.py:542-573): LSB-first pairs
+    u32* cur = c->ws_sel.as<u32>();
+    u32* bufs[2] = {c->ws_ct0.as<u32>(), c->ws_ct1.as<u32>()};
+    for (uint32_t j = 0; j < bits; ++j) {
+      const int C = (int)(d1 >> j);
+      RowsDesc r;
+      r.lo = c->ws_arows.as<u32>() + (size_t)j * ELL * CT;
+      r.lo_b = (size_t)bits_tree * ELL * CT;
+      r.hi = leaves + (size_t)(d0 + j * ELL) * CT;
+      r.hi_b = (size_t)total * CT;
+      r.slot = nullptr;
+      const int mode = (ct_modes && j < n_ct) ? ct_modes[j] : default_mode((size_t)B * C / 2);
+      u32* dst = bufs[j & 1];
+      if ((rc = ext_product(c, cur, (size_t)C, B, C / 2, 1, dst, (size_t)C / 2, r, mode, s, &launches))) return rc;
+      cur = dst;
+    }
+    if (st) CK(cudaEventRecord(c->ev[5], s));
+    *result = cur;
+    if (leaves_out) *leaves_out = leaves;
+    if (st) st->launches += launches;
+    return 0;
+  }
+
+  static int answer_dev(gpir_ctx* c, const gpir_db* db, const u32* d_q, const int32_t* slots, int B,
+                        const uint8_t* eq_modes, uint32_t n_eq, const uint8_t* ct_modes, uint32_t n_ct, u32* d_out,
+                        cudaStream_t s, gpir_stats* st) {
+    const uint32_t d0 = db->d0, d1 = db->d1;
+    const uint32_t total = leaves_of(d0, d1, ELL), bits = ilog2(d1);
+    int rc;
+    if ((rc = check_keys(c, slots, B, stages_of(total), bits > 0))) return rc;
+    if ((rc = ensure_ws(c, B, total, d1, bits))) return rc;
+    if (st) CK(cudaEventRecord(c->ev[0], s));
+    CK(cudaMemcpyAsync(c->ws_kslot.p, slots, (size_t)B * 4, cudaMemcpyHostToDevice, s));
+    if ((rc = bitrev_rows(c, d_q, c->ws_state0.as<u32>(), (size_t)B * 2 * K, s))) return rc;
+    u32* res = nullptr;
+    if (st) st->launches += 2;
+    if ((rc = pipeline(c, db, d1, B, eq_modes, n_eq, ct_modes, n_ct, c->ws_kslot.as<int>(), s, st, &res, nullptr)))
+      return rc;
+    if ((rc = bitrev_rows(c, res, d_out, (size_t)B * 2 * K, s))) return rc;
+    if (st) {
+      CK(cudaEventRecord(c->ev[6], s));
+      CK(cudaEventSynchronize(c->ev[6]));
+      float a;
+      cudaEventElapsedTime(&a, c->ev[1], c->ev[2]);
+      st->ms_expand = a;
+      cudaEventElapsedTime(&a, c->ev[2], c->ev[3]);
+      st->ms_rgsw = a;
+      cudaEventElapsedTime(&a, c->ev[3], c->ev[4]);
+      st->ms_rowsel = a;
+      st->ms_rowsel_kernel = a;
+      cudaEventElapsedTime(&a, c->ev[4], c->ev[5]);
+      st->ms_coltor = a;
+      cudaEventElapsedTime(&a, c->ev[0], c->ev[6]);
+      st->ms_total = a;
+    }
+    return 0;
+  }
+
+  static int check_keys(gpir_ctx* c, const int32_t* slots, int B, uint32_t stages, bool need_rgsw) {
+    for (int b = 0; b < B; ++b) {
+      const int sl = slots[b];
+      if (sl < 0 || (uint32_t)sl >= c->key_slots || c->slot_stages[sl] < 0)
+        FAIL(GPIR_INVALID_STATE, "no uploaded keys for key slot " + std::to_string(sl));
+      if ((uint32_t)c->slot_stages[sl] < stages)
+        FAIL(GPIR_INVALID_STATE, "key slot " + std::to_string(sl) + " has too few evaluation keys");
+      if (need_rgsw && !c->slot_rgsw[sl])
+        FAIL(GPIR_INVALID_STATE, "key slot " + std::to_string(sl) + " has no RGSW of the secret");
+    }
+    return 0;
+  }
+
+  // sharded: expansion over (d0, d1_total), local rowsel + low ColTor on db's columns
+  static int shard_answer(gpir_ctx* c, const gpir_db* db, uint32_t d1_total, const u32* d_q, const int32_t* slots,
+                          int B, u32* d_partials, u32* d_high, cudaStream_t s, gpir_stats* st) {
+    const uint32_t d0 = db->d0;
+    const uint32_t total = leaves_of(d0, d1_total, ELL);
+    const uint32_t bits_tree = ilog2(d1_total), bits = ilog2(db->d1);
+    if (d1_total < db->d1 || (d1_total & (d1_total - 1))) FAIL(GPIR_INVALID_ARGUMENT, "bad d1_total");
+    int rc;
+    if ((rc = check_keys(c, slots, B, stages_of(total), bits_tree > 0))) return rc;
+    if ((rc = ensure_ws(c, B, total, db->d1, bits_tree))) return rc;
+    CK(cudaMemcpyAsync(c->ws_kslot.p, slots, (size_t)B * 4, cudaMemcpyHostToDevice, s));
+    if ((rc = bitrev_rows(c, d_q, c->ws_state0.as<u32>(), (size_t)B * 2 * K, s))) return rc;
+    u32* res = nullptr;
+    u32* leaves = nullptr;
+    if ((rc = pipeline(c, db, d1_total, B, nullptr, 0, nullptr, 0, c->ws_kslot.as<int>(), s, st, &res, &leaves)))
+      return rc;
+    if ((rc = bitrev_rows(c, res, d_partials, (size_t)B * 2 * K, s))) return rc;
+    if (d_high) {
+      const uint32_t nh = bits_tree - bits;
+      for (int b = 0; b < B; ++b)
+        for (uint32_t h = 0; h < nh; ++h) {
+          const uint32_t j = bits + h;
+          u32* dst = d_high + (((size_t)b * nh + h) * 2 * ELL) * CT;
+          const u32* a_rows = c->ws_arows.as<u32>() + ((size_t)b * bits_tree + j) * ELL * CT;
+          const u32* b_rows = leaves + ((size_t)b * total + d0 + j * ELL) * CT;
+          if ((rc = bitrev_rows(c, a_rows, dst, (size_t)ELL * 2 * K, s))) return rc;
+          if ((rc = bitrev_rows(c, b_rows, dst + (size_t)ELL * CT, (size_t)ELL * 2 * K, s))) return rc;
+        }
+    }
+    return 0;
+  }
+
+  static int coltor_dev(gpir_ctx* c, const u32* d_cts, int B, int C, const u32* d_rgsw, u32* d_out, cudaStream_t s) {
+    const uint32_t bits = ilog2((uint32_t)C);
+    int rc;
+    uint32_t launches = 0;
+    // brv copies: cts -> ws_state0, rgsw -> ws_state1 (layout (B, bits, 2 ELL))
+    if ((rc = c->ws_state0.ensure(std::max<size_t>(c->ws_state0.bytes, (size_t)B * C * CT * 4)))) return rc;
+    if ((rc = c->ws_io0.ensure((size_t)B * std::max<uint32_t>(bits, 1) * 2 * ELL * CT * 4))) return rc;
+    if ((rc = c->ws_ct0.ensure(std::max<size_t>(c->ws_ct0.bytes, (size_t)B * std::max(C / 2, 1) * CT * 4)))) return rc;
+    if ((rc = c->ws_ct1.ensure(std::max<size_t>(c->ws_ct1.bytes, (size_t)B * std::max(C / 4, 1) * CT * 4)))) return rc;
+    if ((rc = bitrev_rows(c, d_cts, c->ws_state0.as<u32>(), (size_t)B * C * 2 * K, s))) return rc;
+    if (bits) {
+      if ((rc = bitrev_rows(c, d_rgsw, c->ws_io0.as<u32>(), (size_t)B * bits * 2 * ELL * 2 * K, s))) return rc;
+    }
+    u32* cur = c->ws_state0.as<u32>();
+    u32* bufs[2] = {c->ws_ct0.as<u32>(), c->ws_ct1.as<u32>()};
+    for (uint32_t j = 0; j < bits; ++j) {
+      const int Cj = C >> j;
+      RowsDesc r;
+      r.lo = c->ws_io0.as<u32>() + (size_t)j * 2 * ELL * CT;
+      r.lo_b = (size_t)bits * 2 * ELL * CT;
+      r.hi = r.lo + (size_t)ELL * CT;
+      r.hi_b = r.lo_b;
+      r.slot = nullptr;
+      u32* dst = bufs[j & 1];
+      if ((rc = ext_product(c, cur, (size_t)Cj, B, Cj / 2, 1, dst, (size_t)Cj / 2, r,
+                            default_mode((size_t)B * Cj / 2), s, &launches)))
+        return rc;
+      cur = dst;
+    }
+    return bitrev_rows(c, cur, d_out, (size_t)B * 2 * K, s);
+  }
+
+  // ---- operator-level parity entry points -------------------------------------------
+  static int op_ntt(gpir_ctx* c, const u32* h_in, u32* h_out, uint32_t polys, int inverse);
+  static int op_digits(gpir_ctx* c, const u32* h_coeff, int32_t* h_dig, uint32_t polys);
+  static int op_expand_stage(gpir_ctx* c, const u32* h_state, int B, int C, const u32* h_ksk, int t, int mode,
+                             u32* h_out);
+  static int op_xp(gpir_ctx* c, const u32* h_cts, int B, int M, int pairs, const u32* h_rows, int mode, u32* h_out);
+  static int op_rowsel(gpir_ctx* c, const u32* h_rows, int B, const gpir_db* db, u32* h_out);
+};
+
+// plain NTT rows kernels for the parity entry point
+template <int LOGN, int K>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T) k_ntt_rows(const u32* __restrict__ in, u32* __restrict__ out,
+                                                             int inverse, Tables tb) {
+  constexpr int N = 1 << LOGN;
+  __shared__ __align__(16) u32 xbuf[N];
+  const int row = blockIdx.x;
+  const int i = row % K;
+  const u32* src = in + (size_t)row * N;
+  u32* dst = out + (size_t)row * N;
+  if (inverse) {
+    ntt_inv<LOGN>(
+        xbuf, tb.inv + (size_t)i * N, tb.mod[i], [&](int i0, u32(&x)[16]) { ld16(src + i0, x); },
+        [&](int j, int, u32 v) { dst[j] = v; });
+  } else {
+    ntt_fwd<LOGN>(
+        xbuf, tb.fwd + (size_t)i * N, tb.mod[i].q, [&](int j) -> u32 { return __ldg(src + j); },
+        [&](int i0, const u32(&x)[16]) { st16(dst + i0, x); });
+  }
+}
+
+template <int LOGN, int K, int ELL>
+int Engine<LOGN, K, ELL>::op_ntt(gpir_ctx* c, const u32* h_in, u32* h_out, uint32_t polys, int inverse) {
+  const size_t rows = (size_t)polys * K, words = rows * N;
+  int rc;
+  if ((rc = c->ws_io0.ensure(words * 4)) || (rc = c->ws_io1.ensure(words * 4))) return rc;
+  cudaStream_t s = c->stream;
+  CK(cudaMemcpyAsync(c->ws_io0.p, h_in, words * 4, cudaMemcpyHostToDevice, s));
+  if (inverse) {  // natural NTT values -> brv -> iNTT -> natural coefficients
+    if ((rc = bitrev_rows(c, c->ws_io0.as<u32>(), c->ws_io1.as<u32>(), rows, s))) return rc;
+    k_ntt_rows<LOGN, K><<<(unsigned)rows, T, 0, s>>>(c->ws_io1.as<u32>(), c->ws_io0.as<u32>(), 1, c->tb);
+    CKL();
+    CK(cudaMemcpyAsync(h_out, c->ws_io0.p, words * 4, cudaMemcpyDeviceToHost, s));
+  } else {
+    k_ntt_rows<LOGN, K><<<(unsigned)rows, T, 0, s>>>(c->ws_io0.as<u32>(), c->ws_io1.as<u32>(), 0, c->tb);
+    CKL();
+    if ((rc = bitrev_rows(c, c->ws_io1.as<u32>(), c->ws_io0.as<u32>(), rows, s))) return rc;
+    CK(cudaMemcpyAsync(h_out, c->ws_io0.p, words * 4, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+template <int LOGN, int K, int ELL>
+int Engine<LOGN, K, ELL>::op_digits(gpir_ctx* c, const u32* h_coeff, int32_t* h_dig, uint32_t polys) {
+  int rc;
+  if ((rc = c->ws_io0.ensure((size_t)polys * K * N * 4)) || (rc = c->ws_io1.ensure((size_t)polys * ELL * N * 4)))
+    return rc;
+  cudaStream_t s = c->stream;
+  CK(cudaMemcpyAsync(c->ws_io0.p, h_coeff, (size_t)polys * K * N * 4, cudaMemcpyHostToDevice, s));
+  const size_t tot = (size_t)polys * N;
+  k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->ws_io0.as<u32>(), (int)polys,
+                                                                      c->ws_io1.as<int>(), c->tb, c->cc);
+  CKL();
+  CK(cudaMemcpyAsync(h_dig, c->ws_io1.p, (size_t)polys * ELL * N * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+template <int LOGN, int K, int ELL>
+int Engine<LOGN, K, ELL>::op_expand_stage(gpir_ctx* c, const u32* h_state, int B, int C, const u32* h_ksk, int t,
+                                          int mode, u32* h_out) {
+  int rc;
+  cudaStream_t s = c->stream;
+  DevBuf st, ks, tmp, out;
+  const size_t sw = (size_t)B * C * CT, kw = (size_t)B * ELL * CT, ow = (size_t)B * 2 * C * CT;
+  if ((rc = st.ensure(sw * 4)) || (rc = ks.ensure(kw * 4)) || (rc = tmp.ensure(std::max(sw, kw) * 4)) ||
+      (rc = out.ensure(ow * 4)))
+    return rc;
+  CK(cudaMemcpyAsync(tmp.p, h_state, sw * 4, cudaMemcpyHostToDevice, s));
+  if ((rc = bitrev_rows(c, tmp.as<u32>(), st.as<u32>(), sw >> LOGN, s))) return rc;
+  CK(cudaMemcpyAsync(tmp.p, h_ksk, kw * 4, cudaMemcpyHostToDevice, s));
+  if ((rc = bitrev_rows(c, tmp.as<u32>(), ks.as<u32>(), kw >> LOGN, s))) return rc;
+  RowsDesc r;
+  r.lo = ks.as<u32>();
+  r.lo_b = (size_t)ELL * CT;
+  r.hi = r.lo;
+  r.hi_b = r.lo_b;
+  r.slot = nullptr;
+  uint32_t launches = 0;
+  if ((rc = expand_stage(c, st.as<u32>(), B, C, out.as<u32>(), 2 * C, t, r, mode, s, &launches))) return rc;
+  if ((rc = tmp.ensure(ow * 4))) return rc;
+  if ((rc = bitrev_rows(c, out.as<u32>(), tmp.as<u32>(), ow >> LOGN, s))) return rc;
+  CK(cudaMemcpyAsync(h_out, tmp.p, ow * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  st.release();
+  ks.release();
+  tmp.release();
+  out.release();
+  return 0;
+}
+
+template <int LOGN, int K, int ELL>
+int Engine<LOGN, K, ELL>::op_xp(gpir_ctx* c, const u32* h_cts, int B, int M, int pairs, const u32* h_rows, int mode,
+                                u32* h_out) {
+  int rc;
+  cudaStream_t s = c->stream;
+  const int Min = pairs ? 2 * M : M;
+  DevBuf in, rw, tmp, out;
+  const size_t iw = (size_t)B * Min * CT, rwn = (size_t)B * 2 * ELL * CT, ow = (size_t)B * M * CT;
+  if ((rc = in.ensure(iw * 4)) || (rc = rw.ensure(rwn * 4)) || (rc = tmp.ensure(std::max(iw, rwn) * 4)) ||
+      (rc = out.ensure(ow * 4)))
+    return rc;
+  CK(cudaMemcpyAsync(tmp.p, h_cts, iw * 4, cudaMemcpyHostToDevice, s));
+  if ((rc = bitrev_rows(c, tmp.as<u32>(), in.as<u32>(), iw >> LOGN, s))) return rc;
+  CK(cudaMemcpyAsync(tmp.p, h_rows, rwn * 4, cudaMemcpyHostToDevice, s));
+  if ((rc = bitrev_rows(c, tmp.as<u32>(), rw.as<u32>(), rwn >> LOGN, s))) return rc;
+  RowsDesc r;
+  r.lo = rw.as<u32>();
+  r.lo_b = 2 * (size_t)ELL * CT;
+  r.hi = r.lo + (size_t)ELL * CT;
+  r.hi_b = r.lo_b;
+  r.slot = nullptr;
+  uint32_t launches = 0;
+  if ((rc = ext_product(c, in.as<u32>(), (size_t)Min, B, M, pairs, out.as<u32>(), (size_t)M, r, mode, s, &launches)))
+    return rc;
+  if ((rc = bitrev_rows(c, out.as<u32>(), tmp.as<u32>(), ow >> LOGN, s))) return rc;
+  CK(cudaMemcpyAsync(h_out, tmp.p, ow * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  in.release();
+  rw.release();
+  tmp.release();
+  out.release();
+  return 0;
+}
+
+template <int LOGN, int K, int ELL>
+int Engine<LOGN, K, ELL>::op_rowsel(gpir_ctx* c, const u32* h_rows, int B, const gpir_db* db, u32* h_out) {
+  int rc;
+  cudaStream_t s = c->stream;
+  DevBuf in, tmp, out;
+  const size_t iw = (size_t)B * db->d0 * CT, ow = (size_t)B * db->d1 * CT;
+  if ((rc = in.ensure(iw * 4)) || (rc = tmp.ensure(std::max(iw, ow) * 4)) || (rc = out.ensure(ow * 4))) return rc;
+  CK(cudaMemcpyAsync(tmp.p, h_rows, iw * 4, cudaMemcpyHostToDevice, s));
+  if ((rc = bitrev_rows(c, tmp.as<u32>(), in.as<u32>(), iw >> LOGN, s))) return rc;
+  uint32_t launches = 0;
+  if ((rc = rowsel(c, in.as<u32>(), (size_t)db->d0 * CT, B, db, out.as<u32>(), s, &launches))) return rc;
+  if ((rc = bitrev_rows(c, out.as<u32>(), tmp.as<u32>(), ow >> LOGN, s))) return rc;
+  CK(cudaMemcpyAsync(h_out, tmp.p, ow * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  in.release();
+  tmp.release();
+  out.release();
+  return 0;
+}
+
+// DB encode launcher
+template <int LOGN, int K>
+static int db_encode_launch(gpir_ctx* c, const uint8_t* d_recs, int rec_bytes, int d0, int d1, int plain_bits,
+                            u32* db, cudaStream_t s) {
+  k_db_encode<LOGN, K><<<dim3(d0 * d1, K), NttCfg<LOGN>::T, 0, s>>>(d_recs, rec_bytes, d0, d1, plain_bits, db, c->tb);
+  CKL();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// dispatch over compiled (LOGN, K, ELL) combinations
+
+#define GPIR_COMBOS(X) \
+  X(12, 4, 5)          \
+  X(8, 2, 5)           \
+  X(6, 2, 6)
+
+extern "C" {
+
+const char* gpir_last_error(void) { return g_err.c_str(); }
+const char* gpir_version(void) { return "gpir-b200 0.1 (sm_100a)"; }
+
+int gpir_supported(uint32_t n, uint32_t k, uint32_t ell) {
+  const uint32_t logn = ilog2(n);
+  if ((1u << logn) != n) return 0;
+  const uint32_t key = logn * 10000 + k * 100 + ell;
+#define SUP(L, K_, E) \
+  if (key == L * 10000 + K_ * 100 + E) return 1;
+  GPIR_COMBOS(SUP)
+#undef SUP
+  return 0;
+}
+
+gpir_ctx* gpir_ctx_create(int device, uint32_t n, uint32_t k, const uint32_t* q, const uint32_t* psi, uint32_t z_bits,
+                          uint32_t ell) {
+  if (!gpir_supported(n, k, ell)) {
+    g_err = "unsupported ring/gadget (n=" + std::to_string(n) + ", k=" + std::to_string(k) +
+            ", ell=" + std::to_string(ell) + ") for this build";
+    return nullptr;
+  }
+  if (z_bits < 2 || z_bits > 31 || k > kMaxLimbs || ell > kMaxEll) {
+    g_err = "invalid gadget parameters";
+    return nullptr;
+  }
+  u128 Q = 1;
+  for (uint32_t i = 0; i < k; ++i) {
+    if (q[i] >= (1u << 30)) {
+      g_err = "primes must be below 2^30";
+      return nullptr;
+    }
+    Q *= q[i];
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    g_err = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
+    return nullptr;
+  }
+  gpir_ctx* c = new gpir_ctx();
+  c->device = device;
+  c->n = n;
+  c->logn = ilog2(n);
+  c->k = k;
+  c->ell = ell;
+  c->z_bits = z_bits;
+  c->q.assign(q, q + k);
+  c->psi.assign(psi, psi + k);
+  if (build_tables(c)) {
+    delete c;
+    return nullptr;
+  }
+  cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  for (auto& ev : c->ev) cudaEventCreate(&ev);
+  return c;
+}
+
+void gpir_ctx_destroy(gpir_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (DevBuf* b : {&c->tw_fwd, &c->tw_inv, &c->mono, &c->evk_pool, &c->rgsw_pool, &c->ws_state0, &c->ws_state1,
+                    &c->ws_arows, &c->ws_sel, &c->ws_ct0, &c->ws_ct1, &c->ws_kslot, &c->ws_coeff, &c->ws_dig,
+                    &c->ws_dn, &c->ws_io0, &c->ws_io1})
+    b->release();
+  for (auto& ev : c->ev) cudaEventDestroy(ev);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int gpir_ctx_device(const gpir_ctx* c) { return c ? c->device : -1; }
+
+gpir_db* gpir_db_encode(gpir_ctx* c, const uint8_t* records, uint32_t d0, uint32_t d1, uint32_t record_bytes,
+                        uint32_t plain_bits) {
+  if (!c || !records || !d0 || !d1 || (d1 & (d1 - 1))) {
+    g_err = "invalid database geometry";
+    return nullptr;
+  }
+  if (plain_bits % 8 || plain_bits == 0 || plain_bits > 32 || (uint64_t)record_bytes * 8 > (uint64_t)c->n * plain_bits) {
+    g_err = "record does not fit one plaintext polynomial";
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(c->mu);
+  cudaSetDevice(c->device);
+  gpir_db* db = new gpir_db();
+  db->d0 = d0;
+  db->d1 = d1;
+  const size_t recs = (size_t)d0 * d1;
+  DevBuf raw;
+  int rc = raw.ensure(std::max<size_t>(recs * record_bytes, 16));
+  if (!rc) rc = db->data.ensure(recs * c->k * c->n * 4);
+  if (!rc && cudaMemcpyAsync(raw.p, records, recs * record_bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+    rc = GPIR_CUDA_ERROR, g_err = "db upload failed";
+  if (!rc) {
+    switch (c->logn * 100 + c->k) {
+#define ENC(L, K_, E) \
+  case L * 100 + K_: rc = db_encode_launch<L, K_>(c, raw.as<uint8_t>(), (int)record_bytes, (int)d0, (int)d1, (int)plain_bits, db->data.as<u32>(), c->stream); break;
+      GPIR_COMBOS(ENC)
+#undef ENC
+      default:
+        rc = GPIR_UNSUPPORTED;
+    }
+  }
+  if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = GPIR_CUDA_ERROR, g_err = "db encode failed";
+  raw.release();
+  if (rc) {
+    db->data.release();
+    delete db;
+    return nullptr;
+  }
+  return db;
+}
+
+gpir_db* gpir_db_upload(gpir_ctx* c, const uint32_t* pmajor, uint32_t d0, uint32_t d1) {
+  if (!c || !pmajor || !d0 || !d1 || (d1 & (d1 - 1))) {
+    g_err = "invalid database geometry";
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(c->mu);
+  cudaSetDevice(c->device);
+  gpir_db* db = new gpir_db();
+  db->d0 = d0;
+  db->d1 = d1;
+  const size_t words = (size_t)d0 * d1 * c->k * c->n;
+  DevBuf tmp;
+  int rc = tmp.ensure(words * 4);
+  if (!rc) rc = db->data.ensure(words * 4);
+  if (!rc && cudaMemcpyAsync(tmp.p, pmajor, words * 4, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+    rc = GPIR_CUDA_ERROR, g_err = "db upload failed";
+  if (!rc) rc = bitrev_rows(c, tmp.as<u32>(), db->data.as<u32>(), words >> c->logn, c->stream);
+  if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = GPIR_CUDA_ERROR, g_err = "db upload failed";
+  tmp.release();
+  if (rc) {
+    db->data.release();
+    delete db;
+    return nullptr;
+  }
+  return db;
+}
+
+int gpir_db_download(gpir_ctx* c, const gpir_db* db, uint32_t* out) {
+  if (!c || !db || !out) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  const size_t words = (size_t)db->d0 * db->d1 * c->k * c->n;
+  DevBuf tmp;
+  int rc = tmp.ensure(words * 4);
+  if (rc) return rc;
+  if ((rc = bitrev_rows(c, db->data.as<u32>(), tmp.as<u32>(), words >> c->logn, c->stream))) return rc;
+  CK(cudaMemcpyAsync(out, tmp.p, words * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  tmp.release();
+  return 0;
+}
+
+void gpir_db_destroy(gpir_ctx* c, gpir_db* db) {
+  if (!db) return;
+  if (c) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    db->data.release();
+  }
+  delete db;
+}
+
+size_t gpir_db_bytes(const gpir_db* db) { return db ? db->data.bytes : 0; }
+
+int gpir_keys_put(gpir_ctx* c, int slot, const uint32_t* evks, uint32_t stages, const uint32_t* sk_rgsw) {
+  if (!c || slot < 0 || (stages && !evks)) FAIL(GPIR_INVALID_ARGUMENT, "invalid key upload");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  const size_t CT = c->ct_words();
+  const size_t ell = c->ell;
+  int rc;
+  // grow the pools (slots x max stages), preserving existing keys
+  const uint32_t want_slots = std::max<uint32_t>(c->key_slots, (uint32_t)slot + 1);
+  const uint32_t want_stages = std::max<uint32_t>(c->key_stages, std::max<uint32_t>(stages, 1));
+  if (want_slots != c->key_slots || want_stages != c->key_stages) {
+    const uint32_t ns = std::max<uint32_t>(want_slots, c->key_slots ? 2 * c->key_slots : 4);
+    DevBuf ne, nr;
+    if ((rc = ne.ensure((size_t)ns * want_stages * ell * CT * 4))) return rc;
+    if ((rc = nr.ensure((size_t)ns * 2 * ell * CT * 4))) return rc;
+    for (uint32_t sl = 0; sl < c->key_slots; ++sl) {
+      if (c->slot_stages[sl] > 0)
+        CK(cudaMemcpyAsync(ne.as<u32>() + (size_t)sl * want_stages * ell * CT,
+                           c->evk_pool.as<u32>() + (size_t)sl * c->key_stages * ell * CT,
+                           (size_t)c->slot_stages[sl] * ell * CT * 4, cudaMemcpyDeviceToDevice, c->stream));
+      if (c->slot_rgsw[sl])
+        CK(cudaMemcpyAsync(nr.as<u32>() + (size_t)sl * 2 * ell * CT, c->rgsw_pool.as<u32>() + (size_t)sl * 2 * ell * CT,
+                           2 * ell * CT * 4, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    c->evk_pool.release();
+    c->rgsw_pool.release();
+    c->evk_pool = ne;
+    c->rgsw_pool = nr;
+    ne.p = nullptr;
+    nr.p = nullptr;
+    c->slot_stages.resize(ns, -1);
+    c->slot_rgsw.resize(ns, 0);
+    c->key_slots = ns;
+    c->key_stages = want_stages;
+  }
+  DevBuf tmp;
+  const size_t ew = (size_t)stages * ell * CT, rw = 2 * ell * CT;
+  if ((rc = tmp.ensure(std::max(ew, rw) * 4))) return rc;
+  if (stages) {
+    CK(cudaMemcpyAsync(tmp.p, evks, ew * 4, cudaMemcpyHostToDevice, c->stream));
+    if ((rc = bitrev_rows(c, tmp.as<u32>(), c->evk_pool.as<u32>() + (size_t)slot * c->key_stages * ell * CT,
+                          ew >> c->logn, c->stream)))
+      return rc;
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  c->slot_rgsw[slot] = 0;
+  if (sk_rgsw) {
+    CK(cudaMemcpyAsync(tmp.p, sk_rgsw, rw * 4, cudaMemcpyHostToDevice, c->stream));
+    if ((rc = bitrev_rows(c, tmp.as<u32>(), c->rgsw_pool.as<u32>() + (size_t)slot * rw, rw >> c->logn, c->stream)))
+      return rc;
+    CK(cudaStreamSynchronize(c->stream));
+    c->slot_rgsw[slot] = 1;
+  }
+  c->slot_stages[slot] = (int)stages;
+  tmp.release();
+  return 0;
+}
+
+int gpir_keys_drop(gpir_ctx* c, int slot) {
+  if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (slot >= 0 && (uint32_t)slot < c->key_slots) {
+    c->slot_stages[slot] = -1;
+    c->slot_rgsw[slot] = 0;
+  }
+  return 0;
+}
+
+#define DISPATCH_CASE_ANSWER(L, K_, E) \
+  case L * 10000 + K_ * 100 + E:       \
+    return Engine<L, K_, E>::answer_dev(c, db, d_q, key_slots, (int)B, eq_modes, n_eq, ct_modes, n_ct, d_out, s, stats);
+
+static int answer_dev_dispatch(gpir_ctx* c, const gpir_db* db, const uint32_t* d_q, const int32_t* key_slots,
+                               uint32_t B, const uint8_t* eq_modes, uint32_t n_eq, const uint8_t* ct_modes,
+                               uint32_t n_ct, uint32_t* d_out, cudaStream_t s, gpir_stats* stats) {
+  switch (c->logn * 10000 + c->k * 100 + c->ell) {
+    GPIR_COMBOS(DISPATCH_CASE_ANSWER)
+    default:
+      FAIL(GPIR_UNSUPPORTED, "unsupported combination");
+  }
+}
+
+int gpir_answer_batch_dev(gpir_ctx* c, const gpir_db* db, const uint32_t* d_queries, const int32_t* key_slots,
+                          uint32_t B, const uint8_t* eq_modes, uint32_t n_eq, const uint8_t* ct_modes, uint32_t n_ct,
+                          uint32_t* d_responses, void* stream, gpir_stats* stats) {
+  if (!c || !db || !d_queries || !key_slots || !d_responses) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
+  if (B == 0) return 0;
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  if (stats) memset(stats, 0, sizeof(*stats));
+  int rc = answer_dev_dispatch(c, db, d_queries, key_slots, B, eq_modes, n_eq, ct_modes, n_ct, d_responses, s, stats);
+  if (rc) return rc;
+  if (!stream) CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int gpir_answer_batch(gpir_ctx* c, const gpir_db* db, const uint32_t* queries, const int32_t* key_slots, uint32_t B,
+                      const uint8_t* eq_modes, uint32_t n_eq, const uint8_t* ct_modes, uint32_t n_ct,
+                      uint32_t* responses_out, gpir_stats* stats) {
+  if (!c || !db || !queries || !key_slots || !responses_out) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
+  if (B == 0) return 0;
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const size_t words = (size_t)B * c->ct_words();
+  int rc;
+  if ((rc = c->ws_io0.ensure(words * 4)) || (rc = c->ws_io1.ensure(words * 4))) return rc;
+  if (stats) memset(stats, 0, sizeof(*stats));
+  CK(cudaEventRecord(c->ev[7], s));
+  CK(cudaMemcpyAsync(c->ws_io0.p, queries, words * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaEventRecord(c->ev[8], s));
+  rc = answer_dev_dispatch(c, db, c->ws_io0.as<u32>(), key_slots, B, eq_modes, n_eq, ct_modes, n_ct,
+                           c->ws_io1.as<u32>(), s, stats);
+  if (rc) return rc;
+  CK(cudaEventRecord(c->ev[9], s));
+  CK(cudaMemcpyAsync(responses_out, c->ws_io1.p, words * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaEventRecord(c->ev[10], s));
+  CK(cudaEventSynchronize(c->ev[10]));
+  if (stats) {
+    cudaEventElapsedTime(&stats->ms_h2d, c->ev[7], c->ev[8]);
+    cudaEventElapsedTime(&stats->ms_d2h, c->ev[9], c->ev[10]);
+  }
+  return 0;
+}
+
+int gpir_plan(gpir_ctx* c, uint32_t d0, uint32_t d1, uint32_t B, uint8_t* eq_modes, uint32_t n_eq, uint8_t* ct_modes,
+              uint32_t n_ct) {
+  if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
+  const uint32_t total = leaves_of(d0, d1, c->ell);
+  const uint32_t st = stages_of(total), bits = ilog2(d1);
+  const size_t fill = 2 * 148 * 2;
+  for (uint32_t t = 0; t < n_eq && t < st; ++t)
+    eq_modes[t] = (size_t)B * std::min<uint32_t>(1u << t, total) >= fill ? 1 : 0;
+  for (uint32_t j = 0; j < n_ct && j < bits; ++j) ct_modes[j] = (size_t)B * (d1 >> (j + 1)) >= fill ? 1 : 0;
+  return 0;
+}
+
+#define DISPATCH_CASE_SHARD(L, K_, E) \
+  case L * 10000 + K_ * 100 + E:      \
+    rc = Engine<L, K_, E>::shard_answer(c, db, d1_total, d_queries, key_slots, (int)B, d_partials, d_high_rgsw, s, stats); break;
+
+int gpir_shard_answer(gpir_ctx* c, const gpir_db* db, uint32_t d1_total, const uint32_t* d_queries,
+                      const int32_t* key_slots, uint32_t B, uint32_t* d_partials, uint32_t* d_high_rgsw, void* stream,
+                      gpir_stats* stats) {
+  if (!c || !db || !d_queries || !key_slots || !d_partials) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  if (stats) memset(stats, 0, sizeof(*stats));
+  int rc;
+  switch (c->logn * 10000 + c->k * 100 + c->ell) {
+    GPIR_COMBOS(DISPATCH_CASE_SHARD)
+    default:
+      FAIL(GPIR_UNSUPPORTED, "unsupported combination");
+  }
+  if (rc) return rc;
+  if (!stream) CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+#define DISPATCH_CASE_CT(L, K_, E) \
+  case L * 10000 + K_ * 100 + E:   \
+    rc = Engine<L, K_, E>::coltor_dev(c, d_cts, (int)B, (int)C, d_rgsw, d_out, s); break;
+
+int gpir_coltor_dev(gpir_ctx* c, const uint32_t* d_cts, uint32_t B, uint32_t C, const uint32_t* d_rgsw,
+                    uint32_t* d_out, void* stream) {
+  if (!c || !d_cts || !d_out || !C || (C & (C - 1))) FAIL(GPIR_INVALID_ARGUMENT, "invalid tournament input");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  int rc;
+  switch (c->logn * 10000 + c->k * 100 + c->ell) {
+    GPIR_COMBOS(DISPATCH_CASE_CT)
+    default:
+      FAIL(GPIR_UNSUPPORTED, "unsupported combination");
+  }
+  if (rc) return rc;
+  if (!stream) CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+#define OP_DISPATCH(CALL)                                                   \
+  std::lock_guard<std::mutex> lk(c->mu);                                    \
+  CK(cudaSetDevice(c->device));                                             \
+  switch (c->logn * 10000 + c->k * 100 + c->ell) {                          \
+    case 120405: return Engine<12, 4, 5>::CALL;                             \
+    case 80205: return Engine<8, 2, 5>::CALL;                               \
+    case 60206: return Engine<6, 2, 6>::CALL;                               \
+    default: FAIL(GPIR_UNSUPPORTED, "unsupported combination");             \
+  }
+
+int gpir_op_ntt(gpir_ctx* c, const uint32_t* in, uint32_t* out, uint32_t polys, int inverse) {
+  if (!c || !in || !out) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
+  if (!polys) return 0;
+  OP_DISPATCH(op_ntt(c, in, out, polys, inverse));
+}
+
+int gpir_op_digits(gpir_ctx* c, const uint32_t* coeff, int32_t* digits_out, uint32_t polys) {
+  if (!c || !coeff || !digits_out) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
+  if (!polys) return 0;
+  OP_DISPATCH(op_digits(c, coeff, digits_out, polys));
+}
+
+int gpir_op_expand_stage(gpir_ctx* c, const uint32_t* state, uint32_t B, uint32_t C, const uint32_t* ksk,
+                         uint32_t stage, int mode, uint32_t* out) {
+  if (!c || !state || !ksk || !out || !B || !C) FAIL(GPIR_INVALID_ARGUMENT, "invalid expand_stage input");
+  if (stage >= c->logn) FAIL(GPIR_INVALID_ARGUMENT, "stage out of range");
+  OP_DISPATCH(op_expand_stage(c, state, (int)B, (int)C, ksk, (int)stage, mode, out));
+}
+
+int gpir_op_ext_product(gpir_ctx* c, const uint32_t* cts, uint32_t B, uint32_t M, const uint32_t* rows, int mode,
+                        uint32_t* out) {
+  if (!c || !cts || !rows || !out) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
+  if (!B || !M) return 0;
+  OP_DISPATCH(op_xp(c, cts, (int)B, (int)M, 0, rows, mode, out));
+}
+
+int gpir_op_coltor_stage(gpir_ctx* c, const uint32_t* state, uint32_t B, uint32_t C, const uint32_t* rows, int mode,
+                         uint32_t* out) {
+  if (!c || !state || !rows || !out || C < 2 || (C & 1)) FAIL(GPIR_INVALID_ARGUMENT, "invalid tournament stage input");
+  OP_DISPATCH(op_xp(c, state, (int)B, (int)(C / 2), 1, rows, mode, out));
+}
+
+int gpir_op_rowsel(gpir_ctx* c, const uint32_t* row_cts, uint32_t B, const gpir_db* db, uint32_t* selected) {
+  if (!c || !row_cts || !db || !selected) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
+  if (!B) return 0;
+  OP_DISPATCH(op_rowsel(c, row_cts, (int)B, db, selected));
+}
+
+}  // extern "C"

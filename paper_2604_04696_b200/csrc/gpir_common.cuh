@@ -1,0 +1,99 @@
+// Shared device definitions for the GPIR server pipeline on sm_100a.
+//
+// Data convention: every NTT-domain polynomial
+// limb lives in HBM as n uint32 canonical residues in BIT-REVERSED slot order
+// ("brv layout"): position i holds the evaluation ntt(a)[brv(i)] of the
+// reference's natural-order transform (src/ring.py:6-12).  With that layout the
+// forward transform is a plain Cooley-Tukey DIT (natural coeffs -> brv) and
+// the inverse a Gentleman-Sande DIF (brv -> natural coeffs), so no transform
+// ever permutes through HBM.  Conversion to/from the reference's natural
+// order happens only at the C-ABI boundary.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gpir {
+
+typedef uint32_t u32;
+typedef uint64_t u64;
+
+constexpr int kMaxLimbs = 8;
+constexpr int kMaxEll = 16;
+
+// Per-limb modulus constants.
+struct Modulus {
+  u32 q;
+  u32 qinv_neg;   // -q^{-1} mod 2^32 (Montgomery REDC)
+  u32 r2;         // 2^64 mod q  (REDC(hi * r2) = hi * 2^32 mod q)
+  u32 barrett;    // floor(2^32 / q)
+  u32 ninv;       // n^{-1} mod q
+  u32 ninv_sh;    // Shoup companion of ninv
+  u32 mhat;       // (Q/q)^{-1} mod q   (CRT, src/ring.py:216-220)
+  u32 mhat_sh;
+};
+
+// CRT / gadget constants (src/ring.py:214-235, src/he.py:45-55).
+struct CrtConst {
+  int k;
+  int ell;
+  int z_bits;
+  int logn;
+  u64 m_lo[kMaxLimbs], m_hi[kMaxLimbs];   // Q / q_i as 128-bit
+  u64 q_lo, q_hi;                         // Q
+  u64 half_lo, half_hi;                   // (Q-1)/2
+  int n_red;                              // descending multiples t*Q to subtract
+  u64 red_lo[4], red_hi[4];
+};
+
+// Device-resident transform tables for one context.
+struct Tables {
+  const uint2* fwd;    // [k][n] (psi^brv(i), shoup)     forward CT twiddles
+  const uint2* inv;    // [k][n] (psi^-brv(i), shoup)    inverse GS twiddles
+  Modulus mod[kMaxLimbs];
+};
+
+__device__ __forceinline__ u32 mulhi(u32 a, u32 b) { return __umulhi(a, b); }
+
+// x * w mod q lazily in [0, 2q) for any 32-bit x (Shoup).
+__device__ __forceinline__ u32 mul_shoup(u32 x, u32 w, u32 wsh, u32 q) {
+  return x * w - mulhi(x, wsh) * q;
+}
+
+__device__ __forceinline__ u32 csub(u32 x, u32 m) { return x >= m ? x - m : x; }
+
+// Montgomery REDC: u < q * 2^32  ->  u * 2^-32 mod q in [0, 2q).
+__device__ __forceinline__ u32 redc(u64 u, const Modulus& M) {
+  u32 m = (u32)u * M.qinv_neg;
+  return (u32)((u + (u64)m * M.q) >> 32);
+}
+
+// Any 64-bit value mod q, canonical.
+__device__ __forceinline__ u32 reduce_u64(u64 x, const Modulus& M) {
+  u32 hi = (u32)(x >> 32), lo = (u32)x;
+  u32 a = redc((u64)hi * M.r2, M);                // hi * 2^32 mod q, [0, 2q)
+  u32 b = lo - mulhi(lo, M.barrett) * M.q;        // lo mod q, [0, 2q)
+  u32 r = a + b;                                   // [0, 4q)
+  r = csub(r, 2 * M.q);
+  return csub(r, M.q);
+}
+
+__device__ __forceinline__ u32 mod_add(u32 a, u32 b, u32 q) { return csub(a + b, q); }
+__device__ __forceinline__ u32 mod_sub(u32 a, u32 b, u32 q) { return csub(a + q - b, q); }
+
+__device__ __forceinline__ u32 mod_mul(u32 a, u32 b, const Modulus& M) {
+  return reduce_u64((u64)a * b, M);
+}
+
+__device__ __forceinline__ u32 brv(u32 x, int logn) { return __brev(x) >> (32 - logn); }
+
+// Automorphism X -> X^k_aut as a gather on the brv layout:
+// natural P[j] = (((2j+1) k mod 2n) - 1)/2  (src/ring.py:643-654)
+// brv:  out[i] = in[brv(P[brv(i)])].
+__device__ __forceinline__ u32 aut_src(u32 i, u32 k_aut, int logn) {
+  u32 j = brv(i, logn);
+  u32 two_n_mask = (2u << logn) - 1;
+  u32 e = ((2 * j + 1) * k_aut) & two_n_mask;
+  return brv((e - 1) >> 1, logn);
+}
+
+}  // namespace gpir

@@ -1,0 +1,621 @@
+// GPIR server kernels for sm_100a: ExpandQuery (op-level + stage-fused),
+// external product (op-level + stage-fused, used by RGSW assembly and
+// ColTor), RowSel (CUDA-core, 64-bit lazy accumulation), DB encode and
+// layout conversions.  All NTT-domain data is in the brv layout
+// (gpir_common.cuh).  Template parameters: LOGN = log2 n, K = RNS limbs,
+// ELL = gadget digits.
+#pragma once
+#include "ntt.cuh"
+
+namespace gpir {
+
+#ifndef FUSED_MINB
+#define FUSED_MINB 2
+#endif
+
+// ---------------------------------------------------------------------------
+// BFV row addressing: query b's rows [0, ELL) live at lo, rows [ELL, 2 ELL) at
+// hi, optionally through a per-query key-slot indirection.
+struct RowsDesc {
+  const u32* lo;
+  size_t lo_b;
+  const u32* hi;
+  size_t hi_b;
+  const int* slot;
+  __device__ __forceinline__ const u32* row(int b, int r, int ell, size_t ct) const {
+    const size_t s = slot ? (size_t)slot[b] : (size_t)b;
+    return r < ell ? lo + s * lo_b + (size_t)r * ct : hi + s * hi_b + (size_t)(r - ell) * ct;
+  }
+};
+
+__device__ __forceinline__ void ld16(const u32* __restrict__ p, u32 (&x)[16]) {
+  const uint4* v = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint4 t = __ldg(v + c);
+    x[4 * c] = t.x; x[4 * c + 1] = t.y; x[4 * c + 2] = t.z; x[4 * c + 3] = t.w;
+  }
+}
+
+__device__ __forceinline__ void st16(u32* p, const u32 (&x)[16]) {
+  uint4* v = reinterpret_cast<uint4*>(p);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) v[c] = make_uint4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+}
+
+// acc{0,1}[r] += x[r] * row{a,b}[r] over 16 consecutive brv slots, 4 at a time
+__device__ __forceinline__ void mac16(const u32 (&x)[16], const u32* __restrict__ ra, const u32* __restrict__ rb,
+                                      u64 (&acc0)[16], u64 (&acc1)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(ra) + c);
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(rb) + c);
+    acc0[4 * c] += (u64)x[4 * c] * a.x;
+    acc0[4 * c + 1] += (u64)x[4 * c + 1] * a.y;
+    acc0[4 * c + 2] += (u64)x[4 * c + 2] * a.z;
+    acc0[4 * c + 3] += (u64)x[4 * c + 3] * a.w;
+    acc1[4 * c] += (u64)x[4 * c] * b.x;
+    acc1[4 * c + 1] += (u64)x[4 * c + 1] * b.y;
+    acc1[4 * c + 2] += (u64)x[4 * c + 2] * b.z;
+    acc1[4 * c + 3] += (u64)x[4 * c + 3] * b.w;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CRT + centered digits for one coefficient (src/ring.py:456-495,
+// src/he.py:346-362): exact 128-bit reconstruction into [0, Q), centering to
+// sign/magnitude, then base-2^z_bits digits with the sign-magnitude carry rule.
+template <int K, int ELL>
+__device__ __forceinline__ void dcp_coeff(const u32 (&c)[K], int (&d)[ELL], const Tables& tb, const CrtConst& cc) {
+  typedef unsigned __int128 u128;
+  u128 X = 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const Modulus& M = tb.mod[i];
+    const u32 y = csub(mul_shoup(c[i], M.mhat, M.mhat_sh, M.q), M.q);
+    const u128 m = ((u128)cc.m_hi[i] << 64) | cc.m_lo[i];
+    X += m * y;
+  }
+  for (int t = 0; t < cc.n_red; ++t) {
+    const u128 r = ((u128)cc.red_hi[t] << 64) | cc.red_lo[t];
+    if (X >= r) X -= r;
+  }
+  const u128 half = ((u128)cc.half_hi << 64) | cc.half_lo;
+  const u128 Q = ((u128)cc.q_hi << 64) | cc.q_lo;
+  const bool neg = X > half;
+  u128 mag = neg ? Q - X : X;
+  const int zb = cc.z_bits;
+  const u64 zmask = (1ull << zb) - 1;
+  const int zhalf = 1 << (zb - 1);
+#pragma unroll
+  for (int j = 0; j < ELL; ++j) {
+    int v = (int)((u64)mag & zmask);
+    mag >>= zb;
+    if (j < ELL - 1 && v > zhalf) {
+      v -= 1 << zb;
+      mag += 1;
+    }
+    d[j] = neg ? -v : v;
+  }
+}
+
+__device__ __forceinline__ u32 lift(int d, u32 q) { return d < 0 ? (u32)(d + (int)q) : (u32)d; }
+
+// private (per-thread) smem slot: word index of (slot, r) for this thread
+template <int T>
+__device__ __forceinline__ int pv(int slot, int r) {
+  return (slot * 16 + r) * T + (int)threadIdx.x;
+}
+
+// Dcp over the thread's 16 coefficients, in place in private smem:
+// coefficient limb i at slot i -> digit j at slot j.
+template <int LOGN, int K, int ELL>
+__device__ __forceinline__ void dcp_private(int* priv, const Tables& tb, const CrtConst& cc) {
+  constexpr int T = NttCfg<LOGN>::T;
+#pragma unroll 1
+  for (int r = 0; r < 16; ++r) {
+    u32 c[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) c[i] = (u32)priv[pv<T>(i, r)];
+    int d[ELL];
+    dcp_coeff<K, ELL>(c, d, tb, cc);
+#pragma unroll
+    for (int j = 0; j < ELL; ++j) priv[pv<T>(j, r)] = d[j];
+  }
+}
+
+template <int K, int ELL>
+constexpr int priv_slots() {
+  return K > ELL ? K : ELL;
+}
+
+// ---------------------------------------------------------------------------
+// Stage-fused ExpandQuery node (expand_stage STAGE_LEVEL, src/planner.py:364-380):
+// one CTA per tree node.  Automorphism gather + iNTT of `a` for all limbs,
+// Dcp, then per output limb: ELL digit NTTs, key-switch MAC against the
+// client's evk for this stage, and the (c + s, X^-2^t (c - s)) combine.
+template <int LOGN, int K, int ELL>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
+    k_eq_fused(const u32* __restrict__ state, int C, u32* __restrict__ out, int Cout, RowsDesc ksk, u32 k_aut,
+               const uint2* __restrict__ mono, Tables tb, CrtConst cc) {
+  constexpr int N = 1 << LOGN, T = NttCfg<LOGN>::T, SH = NttCfg<LOGN>::SHIFT;
+  extern __shared__ __align__(16) u32 smem[];
+  u32* xbuf = smem;
+  int* priv = reinterpret_cast<int*>(smem + N);
+  const int tid = threadIdx.x;
+  const int node = blockIdx.x;
+  const int b = node / C, c = node % C;
+  const size_t CT = 2 * (size_t)K * N;
+  const u32* st = state + ((size_t)b * C + c) * CT;
+
+#pragma unroll 1
+  for (int i = 0; i < K; ++i) {
+    __syncthreads();
+    const uint4* src = reinterpret_cast<const uint4*>(st + (size_t)i * N);
+    for (int v = tid; v < N / 4; v += T) reinterpret_cast<uint4*>(xbuf)[v] = __ldg(src + v);
+    __syncthreads();
+    ntt_inv<LOGN>(
+        xbuf, tb.inv + (size_t)i * N, tb.mod[i],
+        [&](int i0, u32(&x)[16]) {
+#pragma unroll
+          for (int r = 0; r < 16; ++r) x[r] = xbuf[aut_src(i0 + r, k_aut, LOGN)];
+        },
+        [&](int, int r, u32 v) { priv[pv<T>(i, r)] = (int)v; });
+  }
+  dcp_private<LOGN, K, ELL>(priv, tb, cc);
+
+  const int i0 = tid << 4;
+  const bool second = c + C < Cout;
+  u32* o0 = out + ((size_t)b * Cout + c) * CT;
+  u32* o1 = out + ((size_t)b * Cout + c + C) * CT;
+#pragma unroll 1
+  for (int i = 0; i < K; ++i) {
+    const Modulus M = tb.mod[i];
+    const u32 q = M.q;
+    u64 acc0[16], acc1[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) acc0[r] = acc1[r] = 0;
+#pragma unroll 1
+    for (int j = 0; j < ELL; ++j) {
+      const u32* ra = ksk.row(b, j, ELL, CT) + (size_t)i * N;
+      const u32* rb = ra + (size_t)K * N;
+      ntt_fwd<LOGN>(
+          xbuf, tb.fwd + (size_t)i * N, q, [&](int jj) -> u32 { return lift(priv[pv<T>(j, jj >> SH)], q); },
+          [&](int, const u32(&x)[16]) {
+            mac16(x, ra + i0, rb + i0, acc0, acc1);
+          });
+    }
+    u32 ca[16], cb[16];
+    ld16(st + (size_t)i * N + i0, ca);
+    ld16(st + (size_t)(K + i) * N + i0, cb);
+    const u32* stb = st + (size_t)(K + i) * N;
+    u32 xa[16], xb[16], ya[16], yb[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const u32 sa = reduce_u64(acc0[r], M);
+      const u32 sb = mod_add(reduce_u64(acc1[r], M), __ldg(stb + aut_src(i0 + r, k_aut, LOGN)), q);
+      xa[r] = mod_add(ca[r], sa, q);
+      xb[r] = mod_add(cb[r], sb, q);
+      const uint2 w = __ldg(&mono[(size_t)i * N + i0 + r]);
+      ya[r] = csub(mul_shoup(mod_sub(ca[r], sa, q), w.x, w.y, q), q);
+      yb[r] = csub(mul_shoup(mod_sub(cb[r], sb, q), w.x, w.y, q), q);
+    }
+    st16(o0 + (size_t)i * N + i0, xa);
+    st16(o0 + (size_t)(K + i) * N + i0, xb);
+    if (second) {
+      st16(o1 + (size_t)i * N + i0, ya);
+      st16(o1 + (size_t)(K + i) * N + i0, yb);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage-fused external product (external_product_batch STAGE_LEVEL,
+// src/planner.py:421-434), one CTA per ciphertext.  With `pairs` the input is
+// the ColTor pair (even, odd) and the CTA computes even + (odd - even) ⊡ rows
+// (coltor_stage, src/planner.py:457-463); otherwise out = in ⊡ rows.
+template <int LOGN, int K, int ELL>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
+    k_xp_fused(const u32* __restrict__ in, size_t in_b, int M_per_b, int pairs, u32* __restrict__ out, size_t out_b,
+               RowsDesc rows, Tables tb, CrtConst cc) {
+  constexpr int N = 1 << LOGN, T = NttCfg<LOGN>::T, SH = NttCfg<LOGN>::SHIFT;
+  extern __shared__ __align__(16) u32 smem[];
+  u32* xbuf = smem;
+  int* priv = reinterpret_cast<int*>(smem + N);
+  const int tid = threadIdx.x;
+  const int b = blockIdx.x / M_per_b, m = blockIdx.x % M_per_b;
+  const size_t CT = 2 * (size_t)K * N;
+  const u32* src = pairs ? in + (b * in_b + 2 * (size_t)m) * CT : in + (b * in_b + (size_t)m) * CT;
+  const u32* odd = src + CT;
+  u32* dst = out + (b * out_b + (size_t)m) * CT;
+  const int i0 = tid << 4;
+
+#pragma unroll 1
+  for (int comp = 0; comp < 2; ++comp) {
+#pragma unroll 1
+    for (int i = 0; i < K; ++i) {
+      const Modulus& Mi = tb.mod[i];
+      const size_t off = (size_t)(comp * K + i) * N;
+      ntt_inv<LOGN>(
+          xbuf, tb.inv + (size_t)i * N, Mi,
+          [&](int j0, u32(&x)[16]) {
+            ld16(src + off + j0, x);
+            if (pairs) {
+              u32 o[16];
+              ld16(odd + off + j0, o);
+#pragma unroll
+              for (int r = 0; r < 16; ++r) x[r] = mod_sub(o[r], x[r], Mi.q);
+            }
+          },
+          [&](int, int r, u32 v) { priv[pv<T>(i, r)] = (int)v; });
+    }
+    dcp_private<LOGN, K, ELL>(priv, tb, cc);
+#pragma unroll 1
+    for (int i = 0; i < K; ++i) {
+      const Modulus Mi = tb.mod[i];
+      const u32 q = Mi.q;
+      u64 acc0[16], acc1[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) acc0[r] = acc1[r] = 0;
+#pragma unroll 1
+      for (int j = 0; j < ELL; ++j) {
+        const u32* ra = rows.row(b, comp * ELL + j, ELL, CT) + (size_t)i * N;
+        const u32* rb = ra + (size_t)K * N;
+        ntt_fwd<LOGN>(
+            xbuf, tb.fwd + (size_t)i * N, q, [&](int jj) -> u32 { return lift(priv[pv<T>(j, jj >> SH)], q); },
+            [&](int, const u32(&x)[16]) {
+              mac16(x, ra + i0, rb + i0, acc0, acc1);
+            });
+      }
+      u32 sa[16], sb[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        sa[r] = reduce_u64(acc0[r], Mi);
+        sb[r] = reduce_u64(acc1[r], Mi);
+      }
+      u32* da = dst + (size_t)i * N + i0;
+      u32* db = dst + (size_t)(K + i) * N + i0;
+      if (comp == 1) {  // add the a-digit half written by this thread in pass 0
+        u32 pa[16], pb[16];
+        ld16(da, pa);
+        ld16(db, pb);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          sa[r] = mod_add(sa[r], pa[r], q);
+          sb[r] = mod_add(sb[r], pb[r], q);
+        }
+        if (pairs) {
+          ld16(src + (size_t)i * N + i0, pa);
+          ld16(src + (size_t)(K + i) * N + i0, pb);
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            sa[r] = mod_add(sa[r], pa[r], q);
+            sb[r] = mod_add(sb[r], pb[r], q);
+          }
+        }
+      }
+      st16(da, sa);
+      st16(db, sb);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Operation-level kernels (expand_stage / external_product_batch
+// OPERATION_LEVEL, src/planner.py:345-363, 406-420): every primitive runs
+// batched over all nodes of a stage and materialises its output.
+
+// (1a) ExpandQuery: automorphism gather + iNTT of `a`; grid (nodes, K).
+template <int LOGN, int K>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T)
+    k_op_eq_intt(const u32* __restrict__ state, int node0, u32 k_aut, u32* __restrict__ coeff, Tables tb) {
+  constexpr int N = 1 << LOGN;
+  __shared__ __align__(16) u32 xbuf[N];
+  const int nd = blockIdx.x, i = blockIdx.y;
+  const u32* row = state + ((size_t)(node0 + nd) * 2 * K + i) * N;
+  u32* dst = coeff + ((size_t)nd * K + i) * N;
+  ntt_inv<LOGN>(
+      xbuf, tb.inv + (size_t)i * N, tb.mod[i],
+      [&](int i0, u32(&x)[16]) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) x[r] = __ldg(row + aut_src(i0 + r, k_aut, LOGN));
+      },
+      [&](int j, int, u32 v) { dst[j] = v; });
+}
+
+// (1b) external product: iNTT of both components (or of odd - even); grid (cts*2, K).
+template <int LOGN, int K>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T)
+    k_op_xp_intt(const u32* __restrict__ in, size_t in_b, int M_per_b, int m0, int pairs, u32* __restrict__ coeff,
+                 Tables tb) {
+  constexpr int N = 1 << LOGN;
+  __shared__ __align__(16) u32 xbuf[N];
+  const int poly = blockIdx.x, i = blockIdx.y;
+  const int ct = poly >> 1, comp = poly & 1;
+  const int g = m0 + ct;
+  const int b = g / M_per_b, m = g % M_per_b;
+  const size_t CT = 2 * (size_t)K * N;
+  const u32* src = pairs ? in + (b * in_b + 2 * (size_t)m) * CT : in + (b * in_b + (size_t)m) * CT;
+  const size_t off = (size_t)(comp * K + i) * N;
+  const u32 q = tb.mod[i].q;
+  u32* dst = coeff + ((size_t)poly * K + i) * N;
+  ntt_inv<LOGN>(
+      xbuf, tb.inv + (size_t)i * N, tb.mod[i],
+      [&](int j0, u32(&x)[16]) {
+        ld16(src + off + j0, x);
+        if (pairs) {
+          u32 o[16];
+          ld16(src + CT + off + j0, o);
+#pragma unroll
+          for (int r = 0; r < 16; ++r) x[r] = mod_sub(o[r], x[r], q);
+        }
+      },
+      [&](int j, int, u32 v) { dst[j] = v; });
+}
+
+// (2) Dcp: one thread per coefficient; coeff [polys][K][N] -> digits [polys][ELL][N].
+template <int LOGN, int K, int ELL>
+__global__ void k_op_dcp(const u32* __restrict__ coeff, int polys, int* __restrict__ digits, Tables tb, CrtConst cc) {
+  constexpr int N = 1 << LOGN;
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (size_t)polys * N) return;
+  const size_t p = g >> LOGN, j = g & (N - 1);
+  u32 c[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) c[i] = __ldg(coeff + (p * K + i) * N + j);
+  int d[ELL];
+  dcp_coeff<K, ELL>(c, d, tb, cc);
+#pragma unroll
+  for (int e = 0; e < ELL; ++e) digits[(p * ELL + e) * N + j] = d[e];
+}
+
+// (3) digit NTT: grid (polys*ELL, K): lift digit mod q_i, forward NTT.
+template <int LOGN, int K>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T)
+    k_op_digit_ntt(const int* __restrict__ digits, u32* __restrict__ dn, Tables tb) {
+  constexpr int N = 1 << LOGN;
+  __shared__ __align__(16) u32 xbuf[N];
+  const int pe = blockIdx.x, i = blockIdx.y;
+  const int* src = digits + (size_t)pe * N;
+  const u32 q = tb.mod[i].q;
+  u32* dst = dn + ((size_t)pe * K + i) * N;
+  ntt_fwd<LOGN>(
+      xbuf, tb.fwd + (size_t)i * N, q, [&](int j) -> u32 { return lift(__ldg(src + j), q); },
+      [&](int i0, const u32(&x)[16]) { st16(dst + i0, x); });
+}
+
+// (4a) ExpandQuery key-switch MAC + combine; one thread per (node, limb, slot).
+template <int LOGN, int K, int ELL>
+__global__ void k_op_eq_mac(const u32* __restrict__ state, int C, int node0, int nodes, const u32* __restrict__ dn,
+                            RowsDesc ksk, u32 k_aut, const uint2* __restrict__ mono, u32* __restrict__ out, int Cout,
+                            Tables tb) {
+  constexpr int N = 1 << LOGN;
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (size_t)nodes * K * N) return;
+  const int pos = (int)(g & (N - 1));
+  const int i = (int)((g >> LOGN) % K);
+  const int nd = (int)(g / ((size_t)K * N));
+  const int gn = node0 + nd;
+  const int b = gn / C, c = gn % C;
+  const size_t CT = 2 * (size_t)K * N;
+  const Modulus M = tb.mod[i];
+  const u32 q = M.q;
+  u64 a0 = 0, a1 = 0;
+#pragma unroll
+  for (int j = 0; j < ELL; ++j) {
+    const u32 d = __ldg(dn + (((size_t)nd * ELL + j) * K + i) * N + pos);
+    const u32* ra = ksk.row(b, j, ELL, CT) + (size_t)i * N + pos;
+    a0 += (u64)d * __ldg(ra);
+    a1 += (u64)d * __ldg(ra + (size_t)K * N);
+  }
+  const u32* st = state + (size_t)gn * CT;
+  const u32 ca = __ldg(st + (size_t)i * N + pos), cb = __ldg(st + (size_t)(K + i) * N + pos);
+  const u32 sa = reduce_u64(a0, M);
+  const u32 sb = mod_add(reduce_u64(a1, M), __ldg(st + (size_t)(K + i) * N + aut_src(pos, k_aut, LOGN)), q);
+  u32* o0 = out + ((size_t)b * Cout + c) * CT;
+  o0[(size_t)i * N + pos] = mod_add(ca, sa, q);
+  o0[(size_t)(K + i) * N + pos] = mod_add(cb, sb, q);
+  if (c + C < Cout) {
+    u32* o1 = out + ((size_t)b * Cout + c + C) * CT;
+    const uint2 w = __ldg(&mono[(size_t)i * N + pos]);
+    o1[(size_t)i * N + pos] = csub(mul_shoup(mod_sub(ca, sa, q), w.x, w.y, q), q);
+    o1[(size_t)(K + i) * N + pos] = csub(mul_shoup(mod_sub(cb, sb, q), w.x, w.y, q), q);
+  }
+}
+
+// (4b) external-product MAC (+ ColTor combine); one thread per (ct, limb, slot).
+template <int LOGN, int K, int ELL>
+__global__ void k_op_xp_mac(const u32* __restrict__ in, size_t in_b, int M_per_b, int m0, int cts, int pairs,
+                            const u32* __restrict__ dn, RowsDesc rows, u32* __restrict__ out, size_t out_b, Tables tb) {
+  constexpr int N = 1 << LOGN;
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (size_t)cts * K * N) return;
+  const int pos = (int)(g & (N - 1));
+  const int i = (int)((g >> LOGN) % K);
+  const int ct = (int)(g / ((size_t)K * N));
+  const int gm = m0 + ct;
+  const int b = gm / M_per_b, m = gm % M_per_b;
+  const size_t CT = 2 * (size_t)K * N;
+  const Modulus M = tb.mod[i];
+  const u32 q = M.q;
+  u64 a0 = 0, a1 = 0;
+#pragma unroll
+  for (int comp = 0; comp < 2; ++comp) {
+#pragma unroll
+    for (int j = 0; j < ELL; ++j) {
+      const u32 d = __ldg(dn + ((((size_t)ct * 2 + comp) * ELL + j) * K + i) * N + pos);
+      const u32* ra = rows.row(b, comp * ELL + j, ELL, CT) + (size_t)i * N + pos;
+      a0 += (u64)d * __ldg(ra);
+      a1 += (u64)d * __ldg(ra + (size_t)K * N);
+    }
+  }
+  u32 sa = reduce_u64(a0, M), sb = reduce_u64(a1, M);
+  if (pairs) {
+    const u32* ev = in + (b * in_b + 2 * (size_t)m) * CT;
+    sa = mod_add(sa, __ldg(ev + (size_t)i * N + pos), q);
+    sb = mod_add(sb, __ldg(ev + (size_t)(K + i) * N + pos), q);
+  }
+  u32* d = out + (b * out_b + (size_t)m) * CT;
+  d[(size_t)i * N + pos] = sa;
+  d[(size_t)(K + i) * N + pos] = sb;
+}
+
+// ---------------------------------------------------------------------------
+// RowSel on CUDA cores (row_select_raw, src/protocol.py:448-492): 4N
+// independent mod-q GEMMs over the p axis, out[b, j, comp, p] =
+// sum_i rows[b, i, comp, p] * db[j, i, p] mod q(p).  P-major operands (p
+// contiguous), one warp lane per p, a CTA covers 32 p x (MT x NT) outputs
+// and streams K in double-buffered cp.async chunks; products accumulate in
+// 64 bits and are folded mod q every 1024 terms (the reference's _k_chunk,
+// src/layout.py:185-187).
+constexpr int RS_MT = 16, RS_NT = 16, RS_KC = 8;
+constexpr int RS_SMEM = 2 * RS_KC * (RS_MT + RS_NT) * 32 * 4;
+
+__device__ __forceinline__ void cp_async16(void* smem_ptr, const void* gptr, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_ptr);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gptr), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NWAIT>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(NWAIT));
+}
+
+__global__ void __launch_bounds__(256)
+    k_rowsel_cc(const u32* __restrict__ A, size_t a_b /* words per query */, int Mrows /* 2B */,
+                const u32* __restrict__ db, int d0, int d1, u32* __restrict__ out, int KN, int logn, Tables tb) {
+  extern __shared__ __align__(16) u32 rs_smem[];
+  u32(*As)[RS_KC][RS_MT][32] = reinterpret_cast<u32(*)[RS_KC][RS_MT][32]>(rs_smem);
+  u32(*Ds)[RS_KC][RS_NT][32] = reinterpret_cast<u32(*)[RS_KC][RS_NT][32]>(rs_smem + 2 * RS_KC * RS_MT * 32);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int mtiles = (Mrows + RS_MT - 1) / RS_MT;
+  const int mt = blockIdx.x % mtiles, nt = blockIdx.x / mtiles;
+  const int p0 = blockIdx.y * 32;
+  const int m0 = mt * RS_MT, n0 = nt * RS_NT;
+  const Modulus M = tb.mod[p0 >> logn];
+  const int mg = warp & 3, ng = warp >> 2;  // thread tile: 4 m x 8 n
+  u64 acc[4][8];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[t][u] = 0;
+
+  auto issue = [&](int stage, int k0) {
+    // A tile: RS_KC x RS_MT rows of 32 words (8 x 16B chunks each) = 1024 chunks
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int ch = tid + it * 256;
+      const int row = ch >> 3, part = ch & 7;
+      const int kk = row / RS_MT, mm = row % RS_MT;
+      const int m = m0 + mm, kidx = k0 + kk;
+      const bool ok = m < Mrows && kidx < d0;
+      const int b = m >> 1, comp = m & 1;
+      const u32* g = A + (ok ? (size_t)b * a_b + ((size_t)kidx * 2 + comp) * KN + p0 + part * 4 : 0);
+      cp_async16(&As[stage][kk][mm][part * 4], ok ? g : A, ok);
+    }
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int ch = tid + it * 256;
+      const int row = ch >> 3, part = ch & 7;
+      const int kk = row / RS_NT, nn = row % RS_NT;
+      const int n = n0 + nn, kidx = k0 + kk;
+      const bool ok = n < d1 && kidx < d0;
+      const u32* g = db + (ok ? ((size_t)n * d0 + kidx) * KN + p0 + part * 4 : 0);
+      cp_async16(&Ds[stage][kk][nn][part * 4], ok ? g : db, ok);
+    }
+    cp_async_commit();
+  };
+
+  const int nk = (d0 + RS_KC - 1) / RS_KC;
+  issue(0, 0);
+  for (int kc = 0; kc < nk; ++kc) {
+    const int s = kc & 1;
+    if (kc + 1 < nk) {
+      issue(s ^ 1, (kc + 1) * RS_KC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < RS_KC; ++kk) {
+      u32 a[4], d[8];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) a[t] = As[s][kk][mg * 4 + t][lane];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) d[u] = Ds[s][kk][ng * 8 + u][lane];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[t][u] += (u64)a[t] * d[u];
+    }
+    if (((kc + 1) * RS_KC) % 1024 == 0) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[t][u] = reduce_u64(acc[t][u], M);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int m = m0 + mg * 4 + t;
+    if (m >= Mrows) continue;
+    const int b = m >> 1, comp = m & 1;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int n = n0 + ng * 8 + u;
+      if (n >= d1) continue;
+      out[(((size_t)b * d1 + n) * 2 + comp) * KN + p0 + lane] = reduce_u64(acc[t][u], M);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// DB preprocessing (encode_database, src/protocol.py:118-153): record bytes
+// -> little-endian base-P words -> centered mod P -> lifted mod q_i ->
+// forward NTT, written straight into the GPU P-major brv layout
+// db[j][i][limb][slot].  grid (records, K).
+template <int LOGN, int K>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T)
+    k_db_encode(const uint8_t* __restrict__ recs, int rec_bytes, int d0, int d1, int plain_bits,
+                u32* __restrict__ db, Tables tb) {
+  constexpr int N = 1 << LOGN;
+  __shared__ __align__(16) u32 xbuf[N];
+  const int r = blockIdx.x, i = blockIdx.y;
+  const int row = r / d1, col = r % d1;
+  const uint8_t* rec = recs + (size_t)r * rec_bytes;
+  const int width = plain_bits / 8;
+  const u32 q = tb.mod[i].q;
+  u32* dst = db + (((size_t)col * d0 + row) * K + i) * N;
+  ntt_fwd<LOGN>(
+      xbuf, tb.fwd + (size_t)i * N, q,
+      [&](int j) -> u32 {
+        u64 w = 0;
+        for (int t = 0; t < width; ++t) {
+          const int o = j * width + t;
+          if (o < rec_bytes) w |= (u64)__ldg(rec + o) << (8 * t);
+        }
+        // center into [-P/2, P/2) then lift (src/protocol.py:145-147)
+        const u64 P = 1ull << plain_bits;
+        if (w >= (P >> 1)) {
+          const u64 neg = P - w;  // |m|, at most P/2 <= 2^31
+          return (u32)((q - (u32)(neg % q)) % q);
+        }
+        return (u32)(w % q);
+      },
+      [&](int i0, const u32(&x)[16]) { st16(dst + i0, x); });
+}
+
+// Bit-reversal permutation of whole limb rows (natural <-> brv; an involution).
+__global__ void k_bitrev_rows(const u32* __restrict__ in, u32* __restrict__ out, size_t rows, int logn) {
+  const size_t n = (size_t)1 << logn;
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= rows * n) return;
+  const size_t row = g >> logn;
+  const u32 j = (u32)(g & (n - 1));
+  out[g] = __ldg(in + row * n + brv(j, logn));
+}
+
+}  // namespace gpir
