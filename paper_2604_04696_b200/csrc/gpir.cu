@@ -14,6 +14,7 @@
 
 #include "../../include/gpir.h"
 #include "kernels.cuh"
+#include "rowsel_tc.cuh"
 
 using namespace gpir;
 
@@ -80,6 +81,8 @@ struct DevBuf {
 struct gpir_db {
   uint32_t d0 = 0, d1 = 0;
   DevBuf data;  // (d1, d0, k, n) brv
+  DevBuf d8;    // tensor-core byte planes D8[p][c][ntile][plane][g][32][16], packed on first use
+  bool d8_ready = false;
 };
 
 struct gpir_ctx {
@@ -88,6 +91,7 @@ struct gpir_ctx {
   std::vector<uint32_t> q, psi;
   Tables tb{};
   CrtConst cc{};
+  TwConst tc{};
   DevBuf tw_fwd, tw_inv, mono;
   // key pool
   uint32_t key_slots = 0, key_stages = 0;
@@ -96,7 +100,9 @@ struct gpir_ctx {
   DevBuf evk_pool, rgsw_pool;
   // workspace
   DevBuf ws_state0, ws_state1, ws_arows, ws_sel, ws_ct0, ws_ct1, ws_kslot;
-  DevBuf ws_coeff, ws_dig, ws_dn, ws_io0, ws_io1;
+  DevBuf ws_coeff, ws_dig, ws_dn, ws_io0, ws_io1, ws_a8;
+  int rowsel_engine = 0;  // 0 auto, 1 CUDA cores, 2 tensor cores
+  int num_sms = 148;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[12];
   std::mutex mu;
@@ -142,6 +148,10 @@ static int build_tables(gpir_ctx* c) {
       const uint32_t w = pw[hbrv(m, c->logn)], iw = ipw[hbrv(m, c->logn)];
       fwd[(size_t)i * n + m] = make_uint2(w, shoup(w, q));
       inv[(size_t)i * n + m] = make_uint2(iw, shoup(iw, q));
+      if (i < (uint32_t)kTwConstLimbs && m < (uint32_t)kTwConstEntries) {
+        c->tc.f[i][m] = fwd[(size_t)i * n + m];
+        c->tc.i[i][m] = inv[(size_t)i * n + m];
+      }
     }
     // X^{-2^t} in brv layout: slot s holds psi^((2 brv(s) + 1) e), e = -2^t mod 2n  (src/ring.py:667-673)
     for (uint32_t t = 0; t < c->logn; ++t) {
@@ -232,7 +242,9 @@ struct Engine {
   static constexpr int N = 1 << LOGN;
   static constexpr int T = NttCfg<LOGN>::T;
   static constexpr size_t CT = 2 * (size_t)K * N;
-  static size_t fused_smem() { return (size_t)N * 4 + (size_t)priv_slots<K, ELL>() * 16 * T * 4; }
+  static size_t fused_smem() {
+    return (size_t)NttCfg<LOGN>::XBUF_WORDS * 4 + (size_t)priv_slots<K, ELL>() * 16 * T * 4;
+  }
 
   static int setup_attrs() {
     static bool done = false;
@@ -258,7 +270,7 @@ struct Engine {
     int rc;
     if (mode == 1) {
       if ((rc = setup_attrs())) return rc;
-      k_eq_fused<LOGN, K, ELL><<<B * C, T, fused_smem(), s>>>(state, C, out, Cout, ksk, k_aut, mono, c->tb, c->cc);
+      k_eq_fused<LOGN, K, ELL><<<B * C, T, fused_smem(), s>>>(state, C, out, Cout, ksk, k_aut, mono, c->tb, c->cc, c->tc);
       CKL();
       ++*launches;
       return 0;
@@ -272,13 +284,13 @@ struct Engine {
     if ((rc = c->ws_dn.ensure(cn * ELL * K * N * 4))) return rc;
     for (size_t n0 = 0; n0 < nodes; n0 += cn) {
       const int nn = (int)std::min(cn, nodes - n0);
-      k_op_eq_intt<LOGN, K><<<dim3(nn, K), T, 0, s>>>(state, (int)n0, k_aut, c->ws_coeff.as<u32>(), c->tb);
+      k_op_eq_intt<LOGN, K><<<dim3(nn, K), T, 0, s>>>(state, (int)n0, k_aut, c->ws_coeff.as<u32>(), c->tb, c->tc);
       CKL();
       const size_t tot = (size_t)nn * N;
       k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), nn,
                                                                           c->ws_dig.as<int>(), c->tb, c->cc);
       CKL();
-      k_op_digit_ntt<LOGN, K><<<dim3(nn * ELL, K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(), c->tb);
+      k_op_digit_ntt<LOGN, K><<<dim3(nn * ELL, K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(), c->tb, c->tc);
       CKL();
       const size_t tm = (size_t)nn * K * N;
       k_op_eq_mac<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(
@@ -296,7 +308,7 @@ struct Engine {
     if (B * M == 0) return 0;
     if (mode == 1) {
       if ((rc = setup_attrs())) return rc;
-      k_xp_fused<LOGN, K, ELL><<<B * M, T, fused_smem(), s>>>(in, in_b, M, pairs, out, out_b, rows, c->tb, c->cc);
+      k_xp_fused<LOGN, K, ELL><<<B * M, T, fused_smem(), s>>>(in, in_b, M, pairs, out, out_b, rows, c->tb, c->cc, c->tc);
       CKL();
       ++*launches;
       return 0;
@@ -310,13 +322,13 @@ struct Engine {
     if ((rc = c->ws_dn.ensure(cn * 2 * ELL * K * N * 4))) return rc;
     for (size_t m0 = 0; m0 < cts; m0 += cn) {
       const int nn = (int)std::min(cn, cts - m0);
-      k_op_xp_intt<LOGN, K><<<dim3(2 * nn, K), T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_coeff.as<u32>(), c->tb);
+      k_op_xp_intt<LOGN, K><<<dim3(2 * nn, K), T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_coeff.as<u32>(), c->tb, c->tc);
       CKL();
       const size_t tot = (size_t)2 * nn * N;
       k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), 2 * nn,
                                                                           c->ws_dig.as<int>(), c->tb, c->cc);
       CKL();
-      k_op_digit_ntt<LOGN, K><<<dim3(2 * nn * ELL, K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(), c->tb);
+      k_op_digit_ntt<LOGN, K><<<dim3(2 * nn * ELL, K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(), c->tb, c->tc);
       CKL();
       const size_t tm = (size_t)nn * K * N;
       k_op_xp_mac<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(in, in_b, M, (int)m0, nn, pairs,
@@ -328,9 +340,60 @@ struct Engine {
     return 0;
   }
 
-  static int rowsel(gpir_ctx* c, const u32* leaves, size_t a_b_words, int B, const gpir_db* db, u32* sel,
-                    cudaStream_t s, uint32_t* launches) {
+  static bool tc_eligible(gpir_ctx* c, int B, const gpir_db* db) {
     const int KN = K * N;
+    if (c->rowsel_engine == 1) return false;
+    return 2 * B <= 128 && db->d0 <= 1024 && KN % 32 == 0;
+  }
+
+  // RowSel: tensor-core path (byte-plane u8 GEMMs, rowsel_tc.cuh) when the
+  // shape allows, else the CUDA-core kernel.  ev_mid (if non-null) is
+  // recorded between operand packing and the GEMM.
+  static int rowsel(gpir_ctx* c, const u32* leaves, size_t a_b_words, int B, gpir_db* db, u32* sel,
+                    cudaStream_t s, uint32_t* launches, cudaEvent_t ev_mid = nullptr) {
+    const int KN = K * N;
+    int rc;
+    if (tc_eligible(c, B, db)) {
+      const int M = 2 * B;
+      const int nchunks = ((int)db->d0 + TC_KC - 1) / TC_KC;
+      const int ntiles = ((int)db->d1 + TC_NT - 1) / TC_NT;
+      if (!db->d8_ready) {
+        if ((rc = db->d8.ensure((size_t)KN * nchunks * ntiles * 4 * TC_NT * TC_KC))) return rc;
+        CK(cudaMemsetAsync(db->d8.p, 0, db->d8.bytes, s));
+        PackSrc ps{db->data.as<u32>(), (size_t)db->d0 * KN, 0, 1, (size_t)KN};
+        dim3 g(KN / 32, (ntiles * TC_NT + 3) / 4, nchunks);
+        k_pack_planes<<<g, 256, 0, s>>>(ps, (int)db->d1, (int)db->d0, KN, TC_NT, ntiles, nchunks,
+                                        db->d8.as<uint8_t>());
+        CKL();
+        db->d8_ready = true;
+      }
+      if ((rc = c->ws_a8.ensure((size_t)KN * nchunks * 4 * M * TC_KC))) return rc;
+      PackSrc pa{leaves, a_b_words, (size_t)KN, 2, 2 * (size_t)KN};
+      dim3 g(KN / 32, (M + 3) / 4, nchunks);
+      k_pack_planes<<<g, 256, 0, s>>>(pa, M, (int)db->d0, KN, M, 1, nchunks, c->ws_a8.as<uint8_t>());
+      CKL();
+      if (ev_mid) CK(cudaEventRecord(ev_mid, s));
+      TcArgs ta;
+      ta.A8 = c->ws_a8.as<uint8_t>();
+      ta.D8 = db->d8.as<uint8_t>();
+      ta.out = sel;
+      ta.M = M;
+      ta.d1 = (int)db->d1;
+      ta.ntiles = ntiles;
+      ta.nchunks = nchunks;
+      ta.KN = KN;
+      ta.logn = LOGN;
+      ta.items = KN * ntiles;
+      const uint32_t stage_bytes = ((4u * M * TC_KC + 4u * TC_NT * TC_KC) + 127u) & ~127u;
+      ta.stages = std::max(2, std::min<int>(TC_MAX_STAGES, (int)((200u * 1024u) / stage_bytes)));
+      const size_t smem = (size_t)ta.stages * stage_bytes + 4096 + 2 * TC_MAX_STAGES * 8 + 4 * 8 + 16;
+      CK(cudaFuncSetAttribute(k_rowsel_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const int grid = std::min(ta.items, c->num_sms);
+      k_rowsel_tc<<<grid, TC_THREADS, smem, s>>>(ta, c->tb);
+      CKL();
+      *launches += 2;
+      return 0;
+    }
     const int mt = (2 * B + RS_MT - 1) / RS_MT, nt = ((int)db->d1 + RS_NT - 1) / RS_NT;
     dim3 grid(mt * nt, KN / 32);
     static bool attr = false;
@@ -338,8 +401,9 @@ struct Engine {
       CK(cudaFuncSetAttribute(k_rowsel_cc, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_SMEM));
       attr = true;
     }
-    k_rowsel_cc<<<grid, 256, RS_SMEM, s>>>(leaves, a_b_words, 2 * B, db->data.as<u32>(), (int)db->d0, (int)db->d1, sel, KN,
-                                     LOGN, c->tb);
+    if (ev_mid) CK(cudaEventRecord(ev_mid, s));
+    k_rowsel_cc<<<grid, 256, RS_SMEM, s>>>(leaves, a_b_words, 2 * B, db->data.as<u32>(), (int)db->d0, (int)db->d1,
+                                           sel, KN, LOGN, c->tb);
     CKL();
     ++*launches;
     return 0;
@@ -406,7 +470,7 @@ struct Engine {
   // Runs expansion over (d0, d1_tree), RGSW assembly for all log2(d1_tree)
   // bits, RowSel on db, and the low log2(db->d1) ColTor stages; returns the
   // pointer to the (B, 1) brv result and the leaves / a-rows for the caller.
-  static int pipeline(gpir_ctx* c, const gpir_db* db, uint32_t d1_tree, int B, const uint8_t* eq_modes, uint32_t n_eq,
+  static int pipeline(gpir_ctx* c, gpir_db* db, uint32_t d1_tree, int B, const uint8_t* eq_modes, uint32_t n_eq,
                       const uint8_t* ct_modes, uint32_t n_ct, const int* kslot, cudaStream_t s, gpir_stats* st,
                       u32** result, u32** leaves_out) {
     const uint32_t d0 = db->d0, d1 = db->d1;
@@ -427,7 +491,9 @@ struct Engine {
         return rc;
     }
     if (st) CK(cudaEventRecord(c->ev[3], s));
-    if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches))) return rc;
+    if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches,
+                     st ? c->ev[11] : nullptr)))
+      return rc;
     if (st) CK(cudaEventRecord(c->ev[4], s));
     // ColTor (src/protocol.py:542-573): LSB-first pairs
     u32* cur = c->ws_sel.as<u32>();
@@ -452,7 +518,7 @@ struct Engine {
     return 0;
   }
 
-  static int answer_dev(gpir_ctx* c, const gpir_db* db, const u32* d_q, const int32_t* slots, int B,
+  static int answer_dev(gpir_ctx* c, gpir_db* db, const u32* d_q, const int32_t* slots, int B,
                         const uint8_t* eq_modes, uint32_t n_eq, const uint8_t* ct_modes, uint32_t n_ct, u32* d_out,
                         cudaStream_t s, gpir_stats* st) {
     const uint32_t d0 = db->d0, d1 = db->d1;
@@ -478,6 +544,7 @@ struct Engine {
       st->ms_rgsw = a;
       cudaEventElapsedTime(&a, c->ev[3], c->ev[4]);
       st->ms_rowsel = a;
+      cudaEventElapsedTime(&a, c->ev[11], c->ev[4]);
       st->ms_rowsel_kernel = a;
       cudaEventElapsedTime(&a, c->ev[4], c->ev[5]);
       st->ms_coltor = a;
@@ -501,7 +568,7 @@ struct Engine {
   }
 
   // sharded: expansion over (d0, d1_total), local rowsel + low ColTor on db's columns
-  static int shard_answer(gpir_ctx* c, const gpir_db* db, uint32_t d1_total, const u32* d_q, const int32_t* slots,
+  static int shard_answer(gpir_ctx* c, gpir_db* db, uint32_t d1_total, const u32* d_q, const int32_t* slots,
                           int B, u32* d_partials, u32* d_high, cudaStream_t s, gpir_stats* st) {
     const uint32_t d0 = db->d0;
     const uint32_t total = leaves_of(d0, d1_total, ELL);
@@ -570,26 +637,28 @@ struct Engine {
   static int op_expand_stage(gpir_ctx* c, const u32* h_state, int B, int C, const u32* h_ksk, int t, int mode,
                              u32* h_out);
   static int op_xp(gpir_ctx* c, const u32* h_cts, int B, int M, int pairs, const u32* h_rows, int mode, u32* h_out);
-  static int op_rowsel(gpir_ctx* c, const u32* h_rows, int B, const gpir_db* db, u32* h_out);
+  static int op_rowsel(gpir_ctx* c, const u32* h_rows, int B, gpir_db* db, u32* h_out);
 };
 
 // plain NTT rows kernels for the parity entry point
 template <int LOGN, int K>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T) k_ntt_rows(const u32* __restrict__ in, u32* __restrict__ out,
-                                                             int inverse, Tables tb) {
+                                                             int inverse, Tables tb,
+                                                             const __grid_constant__ TwConst tc) {
   constexpr int N = 1 << LOGN;
-  __shared__ __align__(16) u32 xbuf[N];
+  __shared__ __align__(16) u32 xbuf[2 * N];
+  NttState ns{xbuf, 0};
   const int row = blockIdx.x;
   const int i = row % K;
   const u32* src = in + (size_t)row * N;
   u32* dst = out + (size_t)row * N;
   if (inverse) {
     ntt_inv<LOGN>(
-        xbuf, tb.inv + (size_t)i * N, tb.mod[i], [&](int i0, u32(&x)[16]) { ld16(src + i0, x); },
+        ns, tb.inv + (size_t)i * N, tc.i[i], tb.mod[i], [&](int i0, u32(&x)[16]) { ld16(src + i0, x); },
         [&](int j, int, u32 v) { dst[j] = v; });
   } else {
     ntt_fwd<LOGN>(
-        xbuf, tb.fwd + (size_t)i * N, tb.mod[i].q, [&](int j) -> u32 { return __ldg(src + j); },
+        ns, tb.fwd + (size_t)i * N, tc.f[i], tb.mod[i], [&](int j) -> u32 { return __ldg(src + j); },
         [&](int i0, const u32(&x)[16]) { st16(dst + i0, x); });
   }
 }
@@ -603,11 +672,11 @@ int Engine<LOGN, K, ELL>::op_ntt(gpir_ctx* c, const u32* h_in, u32* h_out, uint3
   CK(cudaMemcpyAsync(c->ws_io0.p, h_in, words * 4, cudaMemcpyHostToDevice, s));
   if (inverse) {  // natural NTT values -> brv -> iNTT -> natural coefficients
     if ((rc = bitrev_rows(c, c->ws_io0.as<u32>(), c->ws_io1.as<u32>(), rows, s))) return rc;
-    k_ntt_rows<LOGN, K><<<(unsigned)rows, T, 0, s>>>(c->ws_io1.as<u32>(), c->ws_io0.as<u32>(), 1, c->tb);
+    k_ntt_rows<LOGN, K><<<(unsigned)rows, T, 0, s>>>(c->ws_io1.as<u32>(), c->ws_io0.as<u32>(), 1, c->tb, c->tc);
     CKL();
     CK(cudaMemcpyAsync(h_out, c->ws_io0.p, words * 4, cudaMemcpyDeviceToHost, s));
   } else {
-    k_ntt_rows<LOGN, K><<<(unsigned)rows, T, 0, s>>>(c->ws_io0.as<u32>(), c->ws_io1.as<u32>(), 0, c->tb);
+    k_ntt_rows<LOGN, K><<<(unsigned)rows, T, 0, s>>>(c->ws_io0.as<u32>(), c->ws_io1.as<u32>(), 0, c->tb, c->tc);
     CKL();
     if ((rc = bitrev_rows(c, c->ws_io1.as<u32>(), c->ws_io0.as<u32>(), rows, s))) return rc;
     CK(cudaMemcpyAsync(h_out, c->ws_io0.p, words * 4, cudaMemcpyDeviceToHost, s));
@@ -700,7 +769,7 @@ int Engine<LOGN, K, ELL>::op_xp(gpir_ctx* c, const u32* h_cts, int B, int M, int
 }
 
 template <int LOGN, int K, int ELL>
-int Engine<LOGN, K, ELL>::op_rowsel(gpir_ctx* c, const u32* h_rows, int B, const gpir_db* db, u32* h_out) {
+int Engine<LOGN, K, ELL>::op_rowsel(gpir_ctx* c, const u32* h_rows, int B, gpir_db* db, u32* h_out) {
   int rc;
   cudaStream_t s = c->stream;
   DevBuf in, tmp, out;
@@ -723,7 +792,7 @@ int Engine<LOGN, K, ELL>::op_rowsel(gpir_ctx* c, const u32* h_rows, int B, const
 template <int LOGN, int K>
 static int db_encode_launch(gpir_ctx* c, const uint8_t* d_recs, int rec_bytes, int d0, int d1, int plain_bits,
                             u32* db, cudaStream_t s) {
-  k_db_encode<LOGN, K><<<dim3(d0 * d1, K), NttCfg<LOGN>::T, 0, s>>>(d_recs, rec_bytes, d0, d1, plain_bits, db, c->tb);
+  k_db_encode<LOGN, K><<<dim3(d0 * d1, K), NttCfg<LOGN>::T, 0, s>>>(d_recs, rec_bytes, d0, d1, plain_bits, db, c->tb, c->tc);
   CKL();
   return 0;
 }
@@ -764,9 +833,11 @@ gpir_ctx* gpir_ctx_create(int device, uint32_t n, uint32_t k, const uint32_t* q,
     return nullptr;
   }
   u128 Q = 1;
+  const uint32_t logn_ = ilog2(n);
   for (uint32_t i = 0; i < k; ++i) {
-    if (q[i] >= (1u << 30)) {
-      g_err = "primes must be below 2^30";
+    // lazy forward transform bound (values < (2 log2 n + 1) q), as src/ring.py:208-210
+    if ((uint64_t)q[i] * (2 * logn_ + 1) >= (1ull << 32)) {
+      g_err = "prime too large for the lazy 32-bit transform: q * (2 log2 n + 1) must be < 2^32";
       return nullptr;
     }
     Q *= q[i];
@@ -790,6 +861,7 @@ gpir_ctx* gpir_ctx_create(int device, uint32_t n, uint32_t k, const uint32_t* q,
     return nullptr;
   }
   cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   for (auto& ev : c->ev) cudaEventCreate(&ev);
   return c;
 }
@@ -800,7 +872,7 @@ void gpir_ctx_destroy(gpir_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->tw_fwd, &c->tw_inv, &c->mono, &c->evk_pool, &c->rgsw_pool, &c->ws_state0, &c->ws_state1,
                     &c->ws_arows, &c->ws_sel, &c->ws_ct0, &c->ws_ct1, &c->ws_kslot, &c->ws_coeff, &c->ws_dig,
-                    &c->ws_dn, &c->ws_io0, &c->ws_io1})
+                    &c->ws_dn, &c->ws_io0, &c->ws_io1, &c->ws_a8})
     b->release();
   for (auto& ev : c->ev) cudaEventDestroy(ev);
   cudaStreamDestroy(c->stream);
@@ -808,6 +880,13 @@ void gpir_ctx_destroy(gpir_ctx* c) {
 }
 
 int gpir_ctx_device(const gpir_ctx* c) { return c ? c->device : -1; }
+
+int gpir_set_rowsel_engine(gpir_ctx* c, int engine) {
+  if (!c || engine < 0 || engine > 2) FAIL(GPIR_INVALID_ARGUMENT, "engine must be 0 (auto), 1 (CUDA cores) or 2 (tensor cores)");
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->rowsel_engine = engine;
+  return 0;
+}
 
 gpir_db* gpir_db_encode(gpir_ctx* c, const uint8_t* records, uint32_t d0, uint32_t d1, uint32_t record_bytes,
                         uint32_t plain_bits) {
@@ -899,6 +978,7 @@ void gpir_db_destroy(gpir_ctx* c, gpir_db* db) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     db->data.release();
+    db->d8.release();
   }
   delete db;
 }
@@ -976,7 +1056,7 @@ int gpir_keys_drop(gpir_ctx* c, int slot) {
 
 #define DISPATCH_CASE_ANSWER(L, K_, E) \
   case L * 10000 + K_ * 100 + E:       \
-    return Engine<L, K_, E>::answer_dev(c, db, d_q, key_slots, (int)B, eq_modes, n_eq, ct_modes, n_ct, d_out, s, stats);
+    return Engine<L, K_, E>::answer_dev(c, const_cast<gpir_db*>(db), d_q, key_slots, (int)B, eq_modes, n_eq, ct_modes, n_ct, d_out, s, stats);
 
 static int answer_dev_dispatch(gpir_ctx* c, const gpir_db* db, const uint32_t* d_q, const int32_t* key_slots,
                                uint32_t B, const uint8_t* eq_modes, uint32_t n_eq, const uint8_t* ct_modes,
@@ -1046,7 +1126,7 @@ int gpir_plan(gpir_ctx* c, uint32_t d0, uint32_t d1, uint32_t B, uint8_t* eq_mod
 
 #define DISPATCH_CASE_SHARD(L, K_, E) \
   case L * 10000 + K_ * 100 + E:      \
-    rc = Engine<L, K_, E>::shard_answer(c, db, d1_total, d_queries, key_slots, (int)B, d_partials, d_high_rgsw, s, stats); break;
+    rc = Engine<L, K_, E>::shard_answer(c, const_cast<gpir_db*>(db), d1_total, d_queries, key_slots, (int)B, d_partials, d_high_rgsw, s, stats); break;
 
 int gpir_shard_answer(gpir_ctx* c, const gpir_db* db, uint32_t d1_total, const uint32_t* d_queries,
                       const int32_t* key_slots, uint32_t B, uint32_t* d_partials, uint32_t* d_high_rgsw, void* stream,
@@ -1133,7 +1213,7 @@ int gpir_op_coltor_stage(gpir_ctx* c, const uint32_t* state, uint32_t B, uint32_
 int gpir_op_rowsel(gpir_ctx* c, const uint32_t* row_cts, uint32_t B, const gpir_db* db, uint32_t* selected) {
   if (!c || !row_cts || !db || !selected) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
   if (!B) return 0;
-  OP_DISPATCH(op_rowsel(c, row_cts, (int)B, db, selected));
+  OP_DISPATCH(op_rowsel(c, row_cts, (int)B, const_cast<gpir_db*>(db), selected));
 }
 
 }  // extern "C"

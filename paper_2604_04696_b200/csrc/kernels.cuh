@@ -137,11 +137,12 @@ constexpr int priv_slots() {
 template <int LOGN, int K, int ELL>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
     k_eq_fused(const u32* __restrict__ state, int C, u32* __restrict__ out, int Cout, RowsDesc ksk, u32 k_aut,
-               const uint2* __restrict__ mono, Tables tb, CrtConst cc) {
+               const uint2* __restrict__ mono, Tables tb, CrtConst cc, const __grid_constant__ TwConst tc) {
   constexpr int N = 1 << LOGN, T = NttCfg<LOGN>::T, SH = NttCfg<LOGN>::SHIFT;
+  static_assert(K <= kTwConstLimbs, "const twiddle table holds 4 limbs");
   extern __shared__ __align__(16) u32 smem[];
-  u32* xbuf = smem;
-  int* priv = reinterpret_cast<int*>(smem + N);
+  NttState ns{smem, 0};
+  int* priv = reinterpret_cast<int*>(smem + NttCfg<LOGN>::XBUF_WORDS);
   const int tid = threadIdx.x;
   const int node = blockIdx.x;
   const int b = node / C, c = node % C;
@@ -152,13 +153,14 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
   for (int i = 0; i < K; ++i) {
     __syncthreads();
     const uint4* src = reinterpret_cast<const uint4*>(st + (size_t)i * N);
-    for (int v = tid; v < N / 4; v += T) reinterpret_cast<uint4*>(xbuf)[v] = __ldg(src + v);
+    u32* stage_buf = stage_buffer<LOGN>(ns);  // not touched by the next transform
+    for (int v = tid; v < N / 4; v += T) reinterpret_cast<uint4*>(stage_buf)[v] = __ldg(src + v);
     __syncthreads();
     ntt_inv<LOGN>(
-        xbuf, tb.inv + (size_t)i * N, tb.mod[i],
+        ns, tb.inv + (size_t)i * N, tc.i[i], tb.mod[i],
         [&](int i0, u32(&x)[16]) {
 #pragma unroll
-          for (int r = 0; r < 16; ++r) x[r] = xbuf[aut_src(i0 + r, k_aut, LOGN)];
+          for (int r = 0; r < 16; ++r) x[r] = stage_buf[aut_src(i0 + r, k_aut, LOGN)];
         },
         [&](int, int r, u32 v) { priv[pv<T>(i, r)] = (int)v; });
   }
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
       const u32* ra = ksk.row(b, j, ELL, CT) + (size_t)i * N;
       const u32* rb = ra + (size_t)K * N;
       ntt_fwd<LOGN>(
-          xbuf, tb.fwd + (size_t)i * N, q, [&](int jj) -> u32 { return lift(priv[pv<T>(j, jj >> SH)], q); },
+          ns, tb.fwd + (size_t)i * N, tc.f[i], M, [&](int jj) -> u32 { return lift(priv[pv<T>(j, jj >> SH)], q); },
           [&](int, const u32(&x)[16]) {
             mac16(x, ra + i0, rb + i0, acc0, acc1);
           });
@@ -217,11 +219,12 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
 template <int LOGN, int K, int ELL>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
     k_xp_fused(const u32* __restrict__ in, size_t in_b, int M_per_b, int pairs, u32* __restrict__ out, size_t out_b,
-               RowsDesc rows, Tables tb, CrtConst cc) {
+               RowsDesc rows, Tables tb, CrtConst cc, const __grid_constant__ TwConst tc) {
   constexpr int N = 1 << LOGN, T = NttCfg<LOGN>::T, SH = NttCfg<LOGN>::SHIFT;
+  static_assert(K <= kTwConstLimbs, "const twiddle table holds 4 limbs");
   extern __shared__ __align__(16) u32 smem[];
-  u32* xbuf = smem;
-  int* priv = reinterpret_cast<int*>(smem + N);
+  NttState ns{smem, 0};
+  int* priv = reinterpret_cast<int*>(smem + NttCfg<LOGN>::XBUF_WORDS);
   const int tid = threadIdx.x;
   const int b = blockIdx.x / M_per_b, m = blockIdx.x % M_per_b;
   const size_t CT = 2 * (size_t)K * N;
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
       const Modulus& Mi = tb.mod[i];
       const size_t off = (size_t)(comp * K + i) * N;
       ntt_inv<LOGN>(
-          xbuf, tb.inv + (size_t)i * N, Mi,
+          ns, tb.inv + (size_t)i * N, tc.i[i], Mi,
           [&](int j0, u32(&x)[16]) {
             ld16(src + off + j0, x);
             if (pairs) {
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
         const u32* ra = rows.row(b, comp * ELL + j, ELL, CT) + (size_t)i * N;
         const u32* rb = ra + (size_t)K * N;
         ntt_fwd<LOGN>(
-            xbuf, tb.fwd + (size_t)i * N, q, [&](int jj) -> u32 { return lift(priv[pv<T>(j, jj >> SH)], q); },
+            ns, tb.fwd + (size_t)i * N, tc.f[i], Mi, [&](int jj) -> u32 { return lift(priv[pv<T>(j, jj >> SH)], q); },
             [&](int, const u32(&x)[16]) {
               mac16(x, ra + i0, rb + i0, acc0, acc1);
             });
@@ -308,14 +311,16 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
 // (1a) ExpandQuery: automorphism gather + iNTT of `a`; grid (nodes, K).
 template <int LOGN, int K>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T)
-    k_op_eq_intt(const u32* __restrict__ state, int node0, u32 k_aut, u32* __restrict__ coeff, Tables tb) {
+    k_op_eq_intt(const u32* __restrict__ state, int node0, u32 k_aut, u32* __restrict__ coeff, Tables tb,
+                 const __grid_constant__ TwConst tc) {
   constexpr int N = 1 << LOGN;
-  __shared__ __align__(16) u32 xbuf[N];
+  __shared__ __align__(16) u32 xbuf[2 * N];
+  NttState ns{xbuf, 0};
   const int nd = blockIdx.x, i = blockIdx.y;
   const u32* row = state + ((size_t)(node0 + nd) * 2 * K + i) * N;
   u32* dst = coeff + ((size_t)nd * K + i) * N;
   ntt_inv<LOGN>(
-      xbuf, tb.inv + (size_t)i * N, tb.mod[i],
+      ns, tb.inv + (size_t)i * N, tc.i[i], tb.mod[i],
       [&](int i0, u32(&x)[16]) {
 #pragma unroll
         for (int r = 0; r < 16; ++r) x[r] = __ldg(row + aut_src(i0 + r, k_aut, LOGN));
@@ -327,9 +332,10 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
 template <int LOGN, int K>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T)
     k_op_xp_intt(const u32* __restrict__ in, size_t in_b, int M_per_b, int m0, int pairs, u32* __restrict__ coeff,
-                 Tables tb) {
+                 Tables tb, const __grid_constant__ TwConst tc) {
   constexpr int N = 1 << LOGN;
-  __shared__ __align__(16) u32 xbuf[N];
+  __shared__ __align__(16) u32 xbuf[2 * N];
+  NttState ns{xbuf, 0};
   const int poly = blockIdx.x, i = blockIdx.y;
   const int ct = poly >> 1, comp = poly & 1;
   const int g = m0 + ct;
@@ -340,7 +346,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
   const u32 q = tb.mod[i].q;
   u32* dst = coeff + ((size_t)poly * K + i) * N;
   ntt_inv<LOGN>(
-      xbuf, tb.inv + (size_t)i * N, tb.mod[i],
+      ns, tb.inv + (size_t)i * N, tc.i[i], tb.mod[i],
       [&](int j0, u32(&x)[16]) {
         ld16(src + off + j0, x);
         if (pairs) {
@@ -372,15 +378,16 @@ __global__ void k_op_dcp(const u32* __restrict__ coeff, int polys, int* __restri
 // (3) digit NTT: grid (polys*ELL, K): lift digit mod q_i, forward NTT.
 template <int LOGN, int K>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T)
-    k_op_digit_ntt(const int* __restrict__ digits, u32* __restrict__ dn, Tables tb) {
+    k_op_digit_ntt(const int* __restrict__ digits, u32* __restrict__ dn, Tables tb, const __grid_constant__ TwConst tc) {
   constexpr int N = 1 << LOGN;
-  __shared__ __align__(16) u32 xbuf[N];
+  __shared__ __align__(16) u32 xbuf[2 * N];
+  NttState ns{xbuf, 0};
   const int pe = blockIdx.x, i = blockIdx.y;
   const int* src = digits + (size_t)pe * N;
   const u32 q = tb.mod[i].q;
   u32* dst = dn + ((size_t)pe * K + i) * N;
   ntt_fwd<LOGN>(
-      xbuf, tb.fwd + (size_t)i * N, q, [&](int j) -> u32 { return lift(__ldg(src + j), q); },
+      ns, tb.fwd + (size_t)i * N, tc.f[i], tb.mod[i], [&](int j) -> u32 { return lift(__ldg(src + j), q); },
       [&](int i0, const u32(&x)[16]) { st16(dst + i0, x); });
 }
 
@@ -580,9 +587,10 @@ __global__ void __launch_bounds__(256)
 template <int LOGN, int K>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T)
     k_db_encode(const uint8_t* __restrict__ recs, int rec_bytes, int d0, int d1, int plain_bits,
-                u32* __restrict__ db, Tables tb) {
+                u32* __restrict__ db, Tables tb, const __grid_constant__ TwConst tc) {
   constexpr int N = 1 << LOGN;
-  __shared__ __align__(16) u32 xbuf[N];
+  __shared__ __align__(16) u32 xbuf[2 * N];
+  NttState ns{xbuf, 0};
   const int r = blockIdx.x, i = blockIdx.y;
   const int row = r / d1, col = r % d1;
   const uint8_t* rec = recs + (size_t)r * rec_bytes;
@@ -590,7 +598,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
   const u32 q = tb.mod[i].q;
   u32* dst = db + (((size_t)col * d0 + row) * K + i) * N;
   ntt_fwd<LOGN>(
-      xbuf, tb.fwd + (size_t)i * N, q,
+      ns, tb.fwd + (size_t)i * N, tc.f[i], tb.mod[i],
       [&](int j) -> u32 {
         u64 w = 0;
         for (int t = 0; t < width; ++t) {

@@ -109,13 +109,22 @@ def coltor_stage(state, rgsw_rows, basis, gadget, mode, arena=None):
     return out.astype(U64)
 
 
-def row_select(row_cts, db, params):
-    """row_cts (B, d0, 2, k, n) -> selected (B, d1, 2, k, n) on the GPU."""
+_ENGINE_CODES = {"auto": 0, "cudacore": 1, "tensorcore": 2}
+
+
+def row_select(row_cts, db, params, engine: str = "auto"):
+    """row_cts (B, d0, 2, k, n) -> selected (B, d1, 2, k, n) on the GPU.
+
+    engine: "auto" (tensor cores when the shape allows), "cudacore", "tensorcore"."""
     ddb = _device_db(db, params)
+    nat.check(ddb.ctx.lib.gpir_set_rowsel_engine(ddb.ctx.h, _ENGINE_CODES[engine]), "rowsel engine")
     rc = _u32(row_cts)
     B = rc.shape[0]
     if rc.shape[1] != ddb.config.d0:
         raise InvalidArgument(f"expanded row count {rc.shape[1]} != database d0 {ddb.config.d0}")
     out = np.empty((B, ddb.config.d1) + rc.shape[2:], dtype=np.uint32)
-    nat.check(ddb.ctx.lib.gpir_op_rowsel(ddb.ctx.h, nat.ptr(rc), B, ddb.handle, nat.ptr(out)), "rowsel")
+    try:
+        nat.check(ddb.ctx.lib.gpir_op_rowsel(ddb.ctx.h, nat.ptr(rc), B, ddb.handle, nat.ptr(out)), "rowsel")
+    finally:
+        ddb.ctx.lib.gpir_set_rowsel_engine(ddb.ctx.h, 0)
     return out.astype(U64)

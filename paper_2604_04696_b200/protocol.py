@@ -314,7 +314,11 @@ class ServeStats:
         self.phase_seconds[name] = self.phase_seconds.get(name, 0.0) + seconds
 
 
-_ENGINES = ("auto", "cuda", "pmajor", "transposed", "pipeline", "naive")
+# every reference engine name is accepted (all give identical results); on the
+# GPU "cudacore" / "pmajor" / "naive" pin the CUDA-core RowSel kernel and
+# "tensorcore" the tcgen05 one, the rest choose automatically.
+_ENGINES = {"auto": 0, "cuda": 0, "transposed": 0, "pipeline": 0, "pmajor": 1, "naive": 1, "cudacore": 1,
+            "tensorcore": 2}
 
 
 def _modes(config, params, B, hw, plan, mode):
@@ -373,6 +377,7 @@ def answer_batch(queries, keys_by_client, db, params, hw: HardwareModel | None =
         qarr[i, 1] = q.ct.b.limbs
     em, cm = _modes(config, params, B, hw, plan, mode)
     out = np.empty_like(qarr)
+    nat.check(ctx.lib.gpir_set_rowsel_engine(ctx.h, _ENGINES[engine]), "rowsel engine")
     st = nat.GpirStats()
     t0 = time.perf_counter()
     nat.check(ctx.lib.gpir_answer_batch(ctx.h, ddb.handle, nat.ptr(qarr), nat.ptr(slots, nat.C.c_int32), B,

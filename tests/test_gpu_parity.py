@@ -132,6 +132,42 @@ def test_rowsel_golden(G, golden, tag):
     assert np.array_equal(sel, want)
 
 
+@pytest.mark.parametrize("engine", ["cudacore", "tensorcore"])
+@pytest.mark.parametrize("shape", [(1, 5, 2), (3, 64, 33), (32, 70, 64), (64, 256, 40), (17, 129, 1)])
+def test_rowsel_engines_vs_oracle(G, engine, shape):
+    """Both RowSel engines, ragged shapes (B, d0, d1) incl. M = 2B = 128, d0 not a
+    multiple of the 64-byte K chunk, d1 not a multiple of the 32-column tile,
+    and residues at q-1 (largest byte planes)."""
+    from types import SimpleNamespace
+
+    from paper_2604_04696_b200 import ops
+    B, d0, d1 = shape
+    po = O.test_params()
+    p = to_api(po)
+    R = po.ring
+    rng = np.random.default_rng(B * 1000 + d0 + d1)
+    rows = np.stack([rng.integers(0, q, size=(B, d0, 2, R.n), dtype=np.uint64) for q in R.qs], axis=-2)
+    db = np.stack([rng.integers(0, q, size=(d1, d0, R.n), dtype=np.uint64) for q in R.qs], axis=-2)
+    rows[0, 0] = R.q - 1
+    db[0, :] = R.q - 1
+    db = db.reshape(d1, d0, R.k * R.n)
+    fake = SimpleNamespace(config=G.DbConfig(d0, d1, 1), params=p, data=db, layout=G.LayoutKind.P_MAJOR)
+    assert np.array_equal(ops.row_select(rows, fake, p, engine=engine), O.rowsel(rows, db, R))
+
+
+@pytest.mark.parametrize("engine", ["pmajor", "tensorcore"])
+def test_pipeline_rowsel_engines(G, golden, engine):
+    cases, _ = golden
+    case = cases["prod_16x16"]
+    po, records, clients, queries = rebuild_case(case)
+    p = to_api(po)
+    db = G.encode_database(records, G.DbConfig(16, 16, case["record_bytes"]), p)
+    keys = {cid: api_keys(p, c) for cid, c in clients.items()}
+    qs = [api_query(p, q, cid) for q, (cid, _, _) in zip(queries, case["queries"])]
+    out = np.stack([r.ct.raw() for r in G.answer_batch(qs, keys, db, p, engine=engine)])
+    assert digest(out) == case["digest"]["responses"]
+
+
 def test_rowsel_large_k_fold(G):
     """D0 > 1024 exercises the periodic mod-q fold (src/layout.py:185-187)."""
     from types import SimpleNamespace

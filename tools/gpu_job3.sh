@@ -1,0 +1,9 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+for k in ${KERNELS:-k_eq_fused k_xp_fused}; do
+timeout 300 ncu --section SpeedOfLight --section WarpStateStats --section ComputeWorkloadAnalysis --section Occupancy --metrics smsp__inst_executed.sum,gpu__time_duration.sum --clock-control none -k regex:$k -s 3 -c 1 python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_q_$k.txt 2>&1
+done
+tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/bench.log
