@@ -289,7 +289,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches * args.steps,
         "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": words * 4,
                 "d2h_bytes_per_step": words * 4},
-        "roofline": {"kernel": "k_rowsel_cc (RowSel)", "bound": "hbm", "achieved": achieved, "peak": hbm,
+        "roofline": {"kernel": "k_rowsel_tc<64,true> (RowSel, tcgen05 kind::i8)", "bound": "hbm", "achieved": achieved, "peak": hbm,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
                      "algorithmic_bytes": rs_bytes, "avg_launch_ms": rs_ms},
         "clocks": clk.summary(),

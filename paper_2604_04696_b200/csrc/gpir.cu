@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -81,8 +82,8 @@ struct DevBuf {
 struct gpir_db {
   uint32_t d0 = 0, d1 = 0;
   DevBuf data;  // (d1, d0, k, n) brv
-  DevBuf d8;    // tensor-core byte planes D8[p][c][ntile][plane][g][32][16], packed on first use
-  bool d8_ready = false;
+  DevBuf d8;    // tensor-core byte planes D8[p][c][ntile][plane][g][NT][16], packed on first use
+  int d8_nt = 0;
 };
 
 struct gpir_ctx {
@@ -343,7 +344,7 @@ struct Engine {
   static bool tc_eligible(gpir_ctx* c, int B, const gpir_db* db) {
     const int KN = K * N;
     if (c->rowsel_engine == 1) return false;
-    return 2 * B <= 128 && db->d0 <= 1024 && KN % 32 == 0;
+    return 2 * B <= 128 && db->d0 <= 1024 && KN % PK_P == 0;
   }
 
   // RowSel: tensor-core path (byte-plane u8 GEMMs, rowsel_tc.cuh) when the
@@ -355,22 +356,23 @@ struct Engine {
     int rc;
     if (tc_eligible(c, B, db)) {
       const int M = 2 * B;
+      const bool m64 = M <= 64;
+      const int NT = (m64 && db->d1 >= 64) ? 64 : 32;  // two TMEM accumulator buffers either way
       const int nchunks = ((int)db->d0 + TC_KC - 1) / TC_KC;
-      const int ntiles = ((int)db->d1 + TC_NT - 1) / TC_NT;
-      if (!db->d8_ready) {
-        if ((rc = db->d8.ensure((size_t)KN * nchunks * ntiles * 4 * TC_NT * TC_KC))) return rc;
+      const int ntiles = ((int)db->d1 + NT - 1) / NT;
+      if (db->d8_nt != NT) {
+        if ((rc = db->d8.ensure((size_t)KN * nchunks * ntiles * 4 * NT * TC_KC))) return rc;
         CK(cudaMemsetAsync(db->d8.p, 0, db->d8.bytes, s));
         PackSrc ps{db->data.as<u32>(), (size_t)db->d0 * KN, 0, 1, (size_t)KN};
-        dim3 g(KN / 32, (ntiles * TC_NT + 3) / 4, nchunks);
-        k_pack_planes<<<g, 256, 0, s>>>(ps, (int)db->d1, (int)db->d0, KN, TC_NT, ntiles, nchunks,
-                                        db->d8.as<uint8_t>());
+        dim3 g(KN / PK_P, (ntiles * NT + PK_R - 1) / PK_R, nchunks * (TC_KC / PK_K));
+        k_pack_planes<<<g, 256, 0, s>>>(ps, (int)db->d1, (int)db->d0, NT, ntiles, nchunks, db->d8.as<uint8_t>());
         CKL();
-        db->d8_ready = true;
+        db->d8_nt = NT;
       }
       if ((rc = c->ws_a8.ensure((size_t)KN * nchunks * 4 * M * TC_KC))) return rc;
       PackSrc pa{leaves, a_b_words, (size_t)KN, 2, 2 * (size_t)KN};
-      dim3 g(KN / 32, (M + 3) / 4, nchunks);
-      k_pack_planes<<<g, 256, 0, s>>>(pa, M, (int)db->d0, KN, M, 1, nchunks, c->ws_a8.as<uint8_t>());
+      dim3 g(KN / PK_P, (M + PK_R - 1) / PK_R, nchunks * (TC_KC / PK_K));
+      k_pack_planes<<<g, 256, 0, s>>>(pa, M, (int)db->d0, M, 1, nchunks, c->ws_a8.as<uint8_t>());
       CKL();
       if (ev_mid) CK(cudaEventRecord(ev_mid, s));
       TcArgs ta;
@@ -384,13 +386,35 @@ struct Engine {
       ta.KN = KN;
       ta.logn = LOGN;
       ta.items = KN * ntiles;
-      const uint32_t stage_bytes = ((4u * M * TC_KC + 4u * TC_NT * TC_KC) + 127u) & ~127u;
-      ta.stages = std::max(2, std::min<int>(TC_MAX_STAGES, (int)((200u * 1024u) / stage_bytes)));
-      const size_t smem = (size_t)ta.stages * stage_bytes + 4096 + 2 * TC_MAX_STAGES * 8 + 4 * 8 + 16;
-      CK(cudaFuncSetAttribute(k_rowsel_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      const int grid = std::min(ta.items, c->num_sms);
-      k_rowsel_tc<<<grid, TC_THREADS, smem, s>>>(ta, c->tb);
+      const uint32_t stage_bytes = ((4u * M * TC_KC + 4u * NT * TC_KC) + 127u) & ~127u;
+      const size_t outbuf = (size_t)TC_PST * M * (NT + 1) * 4;
+      const size_t fixed = 4096 + outbuf + 2 * TC_MAX_STAGES * 8 + 4 * 8 + 16;
+      ta.stages = std::max(2, std::min<int>(TC_MAX_STAGES, (int)((220u * 1024u - fixed) / stage_bytes)));
+      const size_t smem = (size_t)ta.stages * stage_bytes + fixed;
+      const int grid = std::min(KN / TC_PST, c->num_sms);
+      static const bool prof_on = getenv("GPIR_TC_PROF") != nullptr;
+      DevBuf profbuf;
+      ta.prof = nullptr;
+      if (prof_on) {
+        if ((rc = profbuf.ensure((size_t)grid * 8 * 8))) return rc;
+        CK(cudaMemsetAsync(profbuf.p, 0, profbuf.bytes, s));
+        ta.prof = profbuf.as<unsigned long long>();
+      }
+      auto kern = NT == 64 ? k_rowsel_tc<64, true> : (m64 ? k_rowsel_tc<32, true> : k_rowsel_tc<32, false>);
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<grid, TC_THREADS, smem, s>>>(ta, c->tb);
       CKL();
+      if (prof_on) {
+        std::vector<unsigned long long> h((size_t)grid * 8);
+        CK(cudaMemcpyAsync(h.data(), profbuf.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double sum[8] = {0};
+        for (int g = 0; g < grid; ++g)
+          for (int k = 0; k < 8; ++k) sum[k] += (double)h[(size_t)g * 8 + k] / grid;
+        fprintf(stderr, "[tc prof] avg cycles/CTA: mma_wait_tmem %.0f mma_wait_data %.0f mma_issue %.0f epi_wait %.0f epi_work %.0f\n",
+                sum[0], sum[1], sum[2], sum[3], sum[4]);
+        profbuf.release();
+      }
       *launches += 2;
       return 0;
     }

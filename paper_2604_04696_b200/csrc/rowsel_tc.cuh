@@ -15,19 +15,18 @@
 // stage is two cp.async.bulk copies (UBLKCP):
 //   A8[p][c][plane][g][row m][16 B]          (rows = 2B, packed per batch)
 //   D8[p][c][ntile][plane][g][row 32][16 B]  (rows = DB columns, packed once)
-// Work item = (p, 32-column tile); a persistent CTA per SM runs a multi-stage
+// Work item = (p, NT-column tile, NT = 32 or 64); a persistent CTA per SM runs a multi-stage
 // TMA->MMA pipeline (warp 0 producer, warp 1 single-thread MMA issuer,
-// warps 2-5 epilogue) with two TMEM accumulator buffers (7 x 32 columns
-// each) so the epilogue of one item overlaps the MMAs of the next.
+// warps 2-5 epilogue).  With NT = 32 there are two TMEM accumulator buffers
+// (7 x 32 columns each) so the epilogue of one item overlaps the MMAs of the
+// next; NT = 64 halves the A-operand shared-memory reads per MAC instead.
 #pragma once
 #include "gpir_common.cuh"
 
 namespace gpir {
 
 constexpr int TC_KC = 64;        // K bytes per pipeline stage
-constexpr int TC_NT = 32;        // DB columns per work item (MMA N)
 constexpr int TC_MAX_STAGES = 8;
-constexpr int TC_ACC_COLS = 7 * TC_NT;  // one accumulator buffer
 constexpr int TC_THREADS = 192;  // 6 warps
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -91,6 +90,17 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.b32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -120,45 +130,65 @@ __device__ __forceinline__ size_t pack_src_off(const PackSrc& s, int r) {
 }
 
 // out block of (p, chunk c, [ntile]): dst + ((p * nchunks + c) * ntiles + nt) * (4 * RT * 64)
-// with RT rows per tile (A: RT = R rows, ntiles = 1; D: RT = 32).
+// with RT rows per tile (A: RT = R rows, ntiles = 1; D: RT = 32/64).  One CTA
+// covers 128 p x 4 rows x one 16-byte K group: it reads 64 runs of 512 B and
+// each thread turns 2 rows x 16 k of one p into 4 planes x 32 contiguous bytes.
+constexpr int PK_P = 128, PK_R = 4, PK_K = 16;
 __global__ void __launch_bounds__(256)
-    k_pack_planes(PackSrc src, int R, int Kd, int KN, int RT, int ntiles, int nchunks, uint8_t* __restrict__ dst) {
-  __shared__ u32 tile[4][TC_KC][33];
-  const int p0 = blockIdx.x * 32;
-  const int r0 = blockIdx.y * 4;
-  const int c = blockIdx.z;
+    k_pack_planes(PackSrc src, int R, int Kd, int RT, int ntiles, int nchunks, uint8_t* __restrict__ dst) {
+  __shared__ u32 tile[PK_R][PK_K][PK_P + 1];
+  const int p0 = blockIdx.x * PK_P;
+  const int r0 = blockIdx.y * PK_R;
+  const int kg = blockIdx.z;  // global 16-byte K group
+  const int c = kg / (TC_KC / PK_K), g = kg % (TC_KC / PK_K);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // load: 8 rows x 64 k x 32 p (each warp-instruction reads 128 B of p)
-  for (int it = warp; it < 4 * TC_KC; it += 8) {
-    const int rr = it / TC_KC, kk = it % TC_KC;
-    const int r = r0 + rr, k = c * TC_KC + kk;
-    u32 v = 0;
-    if (r < R && k < Kd) v = __ldg(src.base + pack_src_off(src, r) + (size_t)k * src.k_stride + p0 + lane);
-    tile[rr][kk][lane] = v;
+  uint4 vals[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {  // run index = warp + 8 i: (row, k) pairs, 32 lanes x 16 B = 512 B
+    const int run = warp + 8 * i;
+    const int rr = run / PK_K, kk = run % PK_K;
+    const int r = r0 + rr, k = kg * PK_K + kk;
+    vals[i] = make_uint4(0, 0, 0, 0);
+    if (r < R && k < Kd)
+      vals[i] = __ldg(reinterpret_cast<const uint4*>(src.base + pack_src_off(src, r) + (size_t)k * src.k_stride + p0) +
+                      lane);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int run = warp + 8 * i;
+    u32* t = &tile[run / PK_K][run % PK_K][lane * 4];
+    t[0] = vals[i].x;
+    t[1] = vals[i].y;
+    t[2] = vals[i].z;
+    t[3] = vals[i].w;
   }
   __syncthreads();
-  // store: for each p (32), plane (4), g (4): rows r0..r0+3, 16 B each -> 64 B runs
-  for (int it = tid; it < 32 * 4 * 4 * 4; it += 256) {
-    const int rr = it & 3, g = (it >> 2) & 3, plane = (it >> 4) & 3, pp = it >> 6;
-    const int r = r0 + rr;
-    if (r >= R && r >= ((R + RT - 1) / RT) * RT) continue;
-    uint32_t w[4];
+  const int pp = tid & (PK_P - 1);
+  const int rp = tid >> 7;  // row pair 0/1
+  const int rpad = ((R + RT - 1) / RT) * RT;
+  const int r = r0 + 2 * rp;
+  if (r >= rpad) return;
+  uint32_t w[2][4][4];  // [row][plane][word]
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
-      uint32_t word = 0;
+      u32 v[4];
 #pragma unroll
-      for (int bb = 0; bb < 4; ++bb) {
-        const u32 v = tile[rr][g * 16 + q4 * 4 + bb][pp];
-        word |= ((v >> (8 * plane)) & 0xFFu) << (8 * bb);
-      }
-      w[q4] = word;
+      for (int bb = 0; bb < 4; ++bb) v[bb] = tile[2 * rp + h][q4 * 4 + bb][pp];
+#pragma unroll
+      for (int pl = 0; pl < 4; ++pl)
+        w[h][pl][q4] = __byte_perm(__byte_perm(v[0], v[1], pl | ((pl + 4) << 4)),
+                                   __byte_perm(v[2], v[3], pl | ((pl + 4) << 4)), 0x5410);
     }
-    const int nt = r / RT, rin = r % RT;
-    const size_t blk = (((size_t)(p0 + pp) * nchunks + c) * ntiles + nt) * (size_t)(4 * RT * TC_KC);
-    const size_t off = blk + (size_t)plane * RT * TC_KC + ((size_t)g * RT + rin) * 16;
-    *reinterpret_cast<uint4*>(dst + off) = make_uint4(w[0], w[1], w[2], w[3]);
+  const int nt = r / RT, rin = r % RT;  // rows r, r+1 share the tile (RT even)
+  const size_t blk = (((size_t)(p0 + pp) * nchunks + c) * ntiles + nt) * (size_t)(4 * RT * TC_KC);
+#pragma unroll
+  for (int pl = 0; pl < 4; ++pl) {
+    uint4* d = reinterpret_cast<uint4*>(dst + blk + (size_t)pl * RT * TC_KC + ((size_t)g * RT + rin) * 16);
+    d[0] = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
+    d[1] = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
   }
-  (void)KN;
 }
 
 // ---------------------------------------------------------------------------
@@ -171,9 +201,40 @@ struct TcArgs {
   int d1, ntiles, nchunks, KN, logn;
   int items;          // KN * ntiles
   int stages;         // pipeline depth (<= TC_MAX_STAGES)
+  unsigned long long* prof;  // optional per-CTA cycle counters [grid][8] (GPIR_TC_PROF)
 };
 
+// CTA-local work order: blocks of TC_PST consecutive p (round-robin over
+// CTAs), each block swept over all column tiles, TC_PST items per sweep, so
+// the epilogue can stage TC_PST consecutive p in shared memory and write
+// full 32-byte sectors of the p-innermost output.
+constexpr int TC_PST = 8;
+struct TcSched {
+  int blk, nt, j;
+  __device__ __forceinline__ TcSched() : blk(blockIdx.x), nt(0), j(0) {}
+  __device__ __forceinline__ bool valid(const TcArgs& a) const { return blk * TC_PST < a.KN; }
+  __device__ __forceinline__ int p() const { return blk * TC_PST + j; }
+  __device__ __forceinline__ void next(const TcArgs& a) {
+    if (++j == TC_PST) {
+      j = 0;
+      if (++nt == a.ntiles) {
+        nt = 0;
+        blk += gridDim.x;
+      }
+    }
+  }
+};
+
+// TC_NT: DB columns per work item (= MMA N).  M64: 2B <= 64 uses the M=64
+// MMA shape, whose accumulator rows occupy lanes 0-15 of each TMEM lane
+// quarter, so the two accumulator buffers interleave at lane offsets 0 / 16
+// (same columns) and every epilogue warp owns 16 rows; otherwise M=128 with
+// buffers side by side in columns when 2 * 7 * NT <= 512.
+template <int TC_NT, bool M64>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb) {
+  constexpr int TC_ACC_COLS = 7 * TC_NT;
+  constexpr int NBUF = (M64 || 2 * TC_ACC_COLS <= 512) ? 2 : 1;
+  static_assert(TC_ACC_COLS <= 512, "accumulators exceed TMEM");
   extern __shared__ __align__(1024) uint8_t tc_smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t bytesA = 4u * a.M * TC_KC;
@@ -181,7 +242,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
   const uint32_t stage_bytes = (bytesA + bytesD + 127u) & ~127u;
   uint8_t* stages = tc_smem;
   const int NS = a.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(tc_smem + NS * stage_bytes + 4096);  // +pad: M=128 MMAs over-read
+  u32* outbuf = reinterpret_cast<u32*>(tc_smem + NS * stage_bytes + 4096);  // after the MMA over-read pad
+  const int OB_ROW = TC_NT + 1;  // padded row: conflict-free column writes
+  uint64_t* full = reinterpret_cast<uint64_t*>(outbuf + TC_PST * a.M * OB_ROW);
   uint64_t* empty = full + TC_MAX_STAGES;
   uint64_t* tfull = empty + TC_MAX_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -208,103 +271,136 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  if (warp == 0) {
-    if (lane == 0) {  // producer
-      int s = 0;
-      uint32_t ph = 0;
-      for (int it = blockIdx.x; it < a.items; it += gridDim.x) {
-        const int p = it / a.ntiles, nt = it % a.ntiles;
-        for (int c = 0; c < a.nchunks; ++c) {
-          mbar_wait(&empty[s], ph ^ 1);
+  if (warp == 0) {  // producer: whole warp walks the schedule, one lane issues the bulk copies
+    int s = 0;
+    uint32_t ph = 0;
+    for (TcSched sc; sc.valid(a); sc.next(a)) {
+      const int p = sc.p(), nt = sc.nt;
+      for (int c = 0; c < a.nchunks; ++c) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (elect_one()) {
           uint8_t* sa = stages + s * stage_bytes;
           mbar_expect_tx(&full[s], bytesA + bytesD);
           bulk_g2s(sa, a.A8 + ((size_t)p * a.nchunks + c) * bytesA, bytesA, &full[s]);
           bulk_g2s(sa + bytesA, a.D8 + (((size_t)p * a.nchunks + c) * a.ntiles + nt) * bytesD, bytesD, &full[s]);
-          if (++s == NS) {
-            s = 0;
-            ph ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1;
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer
-      constexpr uint32_t idesc = umma_idesc_u8(128, TC_NT);
-      int s = 0;
-      uint32_t ph = 0;
-      int local = 0;
-      for (int it = blockIdx.x; it < a.items; it += gridDim.x, ++local) {
-        const int ab = local & 1;
-        const uint32_t aph = (local >> 1) & 1;
-        mbar_wait(&tempty[ab], aph ^ 1);
+  } else if (warp == 1) {  // MMA issuer: converged warp, one elected lane issues tcgen05.mma
+    constexpr uint32_t idesc = umma_idesc_u8(M64 ? 64 : 128, TC_NT);
+    int s = 0;
+    uint32_t ph = 0;
+    int local = 0;
+    const uint32_t a_ks = (2u * a.M * 16u) >> 4;         // descriptor step of one 32-byte K step
+    const uint32_t a_pl = (uint32_t)(a.M * TC_KC) >> 4;  // ... of one byte plane
+    for (TcSched sc; sc.valid(a); sc.next(a), ++local) {
+      const int ab = (NBUF == 2) ? (local & 1) : 0;
+      const uint32_t aph = (NBUF == 2) ? ((local >> 1) & 1) : (local & 1);
+      long long t0 = clock64();
+      mbar_wait(&tempty[ab], aph ^ 1);
+      long long t1 = clock64();
+      if (a.prof && lane == 0) a.prof[blockIdx.x * 8 + 0] += t1 - t0;  // MMA waits for TMEM
+      tc_fence_after();
+      const uint32_t dcol = M64 ? tbase + ((uint32_t)(16 * ab) << 16) : tbase + ab * TC_ACC_COLS;
+      for (int c = 0; c < a.nchunks; ++c) {
+        long long t2 = clock64();
+        mbar_wait(&full[s], ph);
+        long long t3 = clock64();
+        if (a.prof && lane == 0) a.prof[blockIdx.x * 8 + 1] += t3 - t2;  // MMA waits for data
         tc_fence_after();
-        const uint32_t dcol = tbase + ab * TC_ACC_COLS;
-        uint32_t inited = 0;
-        for (int c = 0; c < a.nchunks; ++c) {
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
+        if (elect_one()) {
           const uint32_t sa = smem_u32(stages + s * stage_bytes);
-          const uint32_t sd = sa + bytesA;
-#pragma unroll 1
+          const uint64_t a0 = umma_desc(sa, a.M * 16, 128);
+          const uint64_t b0 = umma_desc(sa + bytesA, TC_NT * 16, 128);
+#pragma unroll
           for (int ks = 0; ks < TC_KC / 32; ++ks) {
 #pragma unroll
             for (int sp = 0; sp < 4; ++sp) {
 #pragma unroll
               for (int tp = 0; tp < 4; ++tp) {
                 const int u = sp + tp;
-                const uint64_t ad = umma_desc(sa + sp * a.M * TC_KC + ks * 2 * a.M * 16, a.M * 16, 128);
-                const uint64_t bd = umma_desc(sd + tp * TC_NT * TC_KC + ks * 2 * TC_NT * 16, TC_NT * 16, 128);
-                umma_i8(dcol + u * TC_NT, ad, bd, idesc, (inited >> u) & 1);
-                inited |= 1u << u;
+                const bool first = (ks == 0) && (sp == (u > 3 ? u - 3 : 0));  // first product into diagonal u
+                const uint64_t ad = a0 + (uint64_t)(sp * a_pl + ks * a_ks);
+                const uint64_t bd = b0 + (uint64_t)((tp * TC_NT * TC_KC + ks * 2 * TC_NT * 16) >> 4);
+                umma_i8(dcol + u * TC_NT, ad, bd, idesc, (c > 0 || !first) ? 1u : 0u);
               }
             }
           }
           umma_commit(&empty[s]);  // smem stage free once these MMAs retire
-          if (++s == NS) {
-            s = 0;
-            ph ^= 1;
-          }
+          if (c == a.nchunks - 1) umma_commit(&tfull[ab]);
         }
-        umma_commit(&tfull[ab]);
+        __syncwarp();
+        if (a.prof && lane == 0) a.prof[blockIdx.x * 8 + 2] += clock64() - t3;  // MMA issue
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1;
+        }
       }
     }
   } else {  // epilogue warps 2..5: TMEM lanes 32*(warp%4) .. +31
     const int quad = warp & 3;
-    const int m = quad * 32 + lane;
+    const int etid = (warp - 2) * 32 + lane;  // 0..127
     int local = 0;
-    for (int it = blockIdx.x; it < a.items; it += gridDim.x, ++local) {
-      const int ab = local & 1;
-      const uint32_t aph = (local >> 1) & 1;
-      const int p = it / a.ntiles, nt = it % a.ntiles;
+    for (TcSched sc; sc.valid(a); sc.next(a), ++local) {
+      const int ab = (NBUF == 2) ? (local & 1) : 0;
+      const uint32_t aph = (NBUF == 2) ? ((local >> 1) & 1) : (local & 1);
+      const int p = sc.p(), nt = sc.nt;
+      long long e0 = clock64();
       mbar_wait(&tfull[ab], aph);
+      long long e1 = clock64();
+      if (a.prof && lane == 0 && quad == 0) a.prof[blockIdx.x * 8 + 3] += e1 - e0;  // epilogue waits
       tc_fence_after();
-      const Modulus M = tb.mod[p >> a.logn];
-      const uint32_t tl = tbase + ((uint32_t)(quad * 32) << 16) + ab * TC_ACC_COLS;
+      // row held by this thread's TMEM lane for accumulator buffer ab
+      const int m = M64 ? quad * 16 + (lane & 15) : quad * 32 + lane;
+      const bool mine = M64 ? ((lane >> 4) == ab) : true;
+      if ((M64 ? quad * 16 : quad * 32) < a.M) {
+        const Modulus M = tb.mod[p >> a.logn];
+        const uint32_t tl = M64 ? tbase + ((uint32_t)(quad * 32) << 16)
+                                : tbase + ((uint32_t)(quad * 32) << 16) + ab * TC_ACC_COLS;
+        u32* orow = outbuf + ((size_t)sc.j * a.M + m) * OB_ROW;
 #pragma unroll 1
-      for (int c8 = 0; c8 < TC_NT; c8 += 8) {
-        u64 acc[8];
+        for (int c8 = 0; c8 < TC_NT; c8 += 8) {
+          uint32_t v[7][8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = 0;
-#pragma unroll
-        for (int u = 0; u < 7; ++u) {
-          uint32_t v[8];
-          tmem_ld8(tl + u * TC_NT + c8, v);
+          for (int u = 0; u < 7; ++u) tmem_ld8(tl + u * TC_NT + c8, v[u]);
           tmem_ld_wait();
+          if (mine && m < a.M) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] += (u64)v[j] << (8 * u);
-        }
-        if (m < a.M) {
-          const int b = m >> 1, comp = m & 1;
+            for (int j = 0; j < 8; ++j) {
+              u64 acc = 0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int n = nt * TC_NT + c8 + j;
-            if (n < a.d1) a.out[(((size_t)b * a.d1 + n) * 2 + comp) * a.KN + p] = reduce_u64(acc[j], M);
+              for (int u = 0; u < 7; ++u) acc += (u64)v[u][j] << (8 * u);
+              orow[c8 + j] = reduce_u64(acc, M);
+            }
           }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[ab]);
+      if (lane == 0) mbar_arrive(&tempty[ab]);  // TMEM buffer free; staging continues
+      if (sc.j == TC_PST - 1) {                 // flush TC_PST consecutive p as 32-byte runs
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int p0 = sc.blk * TC_PST;
+        for (int w = etid; w < a.M * TC_NT; w += 128) {
+          const int mm = w / TC_NT, cc = w % TC_NT;
+          const int n = nt * TC_NT + cc;
+          if (n < a.d1) {
+            u32 o[TC_PST];
+#pragma unroll
+            for (int j = 0; j < TC_PST; ++j) o[j] = outbuf[((size_t)j * a.M + mm) * OB_ROW + cc];
+            uint4* dst = reinterpret_cast<uint4*>(a.out + (((size_t)(mm >> 1) * a.d1 + n) * 2 + (mm & 1)) * a.KN + p0);
+            dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+            dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+      if (a.prof && lane == 0 && quad == 0) a.prof[blockIdx.x * 8 + 4] += clock64() - e1;  // epilogue work
     }
   }
   __syncthreads();
