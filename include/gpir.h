@@ -7,8 +7,7 @@
  *                    src/protocol.py:165-199   -> gpir_keys_put
  *   answer_batch     src/protocol.py:635-682   -> gpir_answer_batch (host buffers)
  *                                               gpir_answer_batch_dev (device buffers)
- *   expand_query_batch src/protocol.py:322-367 -> gpir_expand_dev
- *   row_select_raw   src/protocol.py:448-492   -> gpir_rowsel_dev
+ *   cluster._answer_shard src/cluster.py:252-265 -> gpir_shard_answer
  *   col_tournament_batch src/protocol.py:542-573 -> gpir_coltor_dev
  * Operator-level parity entry points (host buffers, reference natural order):
  *   ntt_raw / intt_raw      src/ring.py:408-453     -> gpir_op_ntt
@@ -24,7 +23,9 @@
  * return 0 on success, a negative gpir_status otherwise; gpir_last_error()
  * gives the message (thread-local).  Contexts are thread-safe (one internal
  * mutex per context).  Stage modes: 0 = operation-level, 1 = stage-fused
- * (planner.ExecMode OPERATION_LEVEL / STAGE_LEVEL, src/planner.py:105-107).
+ * (planner.ExecMode OPERATION_LEVEL / STAGE_LEVEL, src/planner.py:105-107),
+ * 2 = split stage-fused (per-node iNTT+Dcp kernel, per node x limb NTT+MAC
+ * kernel; experimental, bit-identical).
  */
 #ifndef GPIR_H
 #define GPIR_H

@@ -16,6 +16,7 @@
 #include "../../include/gpir.h"
 #include "kernels.cuh"
 #include "rowsel_tc.cuh"
+#include "stage_kernels.cuh"
 
 using namespace gpir;
 
@@ -253,6 +254,10 @@ struct Engine {
     const int sm = (int)fused_smem();
     CK(cudaFuncSetAttribute(k_eq_fused<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_xp_fused<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute(k_eq_nttmac<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)k2_smem_bytes<LOGN>()));
+    CK(cudaFuncSetAttribute(k_xp_nttmac<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)k2_smem_bytes<LOGN>()));
     done = true;
     return 0;
   }
@@ -269,11 +274,27 @@ struct Engine {
     const u32 k_aut = (u32)(N >> t) + 1;
     const uint2* mono = c->mono.as<uint2>() + (size_t)t * K * N;
     int rc;
-    if (mode == 1) {
+    if (mode == 1) {  // stage-fused: one CTA per node (all limbs and digits resident in shared memory)
       if ((rc = setup_attrs())) return rc;
       k_eq_fused<LOGN, K, ELL><<<B * C, T, fused_smem(), s>>>(state, C, out, Cout, ksk, k_aut, mono, c->tb, c->cc, c->tc);
       CKL();
       ++*launches;
+      return 0;
+    }
+    if (mode == 2) {  // split stage-fused: K1 (iNTT + Dcp per node) -> K2 (digit NTT + MAC + combine per node x limb)
+      if ((rc = setup_attrs())) return rc;
+      const size_t nodes = (size_t)B * C;
+      const size_t cn = std::min(nodes, op_chunk((size_t)ELL * N));
+      if ((rc = c->ws_dig.ensure(cn * ELL * N * 4))) return rc;
+      for (size_t n0 = 0; n0 < nodes; n0 += cn) {
+        const int nn = (int)std::min(cn, nodes - n0);
+        k_eq_dcp<LOGN, K, ELL><<<nn, T, 0, s>>>(state, (int)n0, k_aut, c->ws_dig.as<int>(), c->tb, c->cc, c->tc);
+        CKL();
+        k_eq_nttmac<LOGN, K, ELL><<<nn * K, T, k2_smem_bytes<LOGN>(), s>>>(
+            state, C, (int)n0, c->ws_dig.as<int>(), ksk, k_aut, mono, out, Cout, c->tb, c->tc);
+        CKL();
+        *launches += 2;
+      }
       return 0;
     }
     const size_t per = (size_t)K * N + (size_t)ELL * N + (size_t)ELL * K * N;
@@ -312,6 +333,23 @@ struct Engine {
       k_xp_fused<LOGN, K, ELL><<<B * M, T, fused_smem(), s>>>(in, in_b, M, pairs, out, out_b, rows, c->tb, c->cc, c->tc);
       CKL();
       ++*launches;
+      return 0;
+    }
+    if (mode == 2) {
+      if ((rc = setup_attrs())) return rc;
+      const size_t cts = (size_t)B * M;
+      const size_t cn = std::min(cts, op_chunk((size_t)2 * ELL * N));
+      if ((rc = c->ws_dig.ensure(cn * 2 * ELL * N * 4))) return rc;
+      for (size_t m0 = 0; m0 < cts; m0 += cn) {
+        const int nn = (int)std::min(cn, cts - m0);
+        k_xp_dcp<LOGN, K, ELL><<<nn, T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_dig.as<int>(), c->tb, c->cc, c->tc);
+        CKL();
+        k_xp_nttmac<LOGN, K, ELL><<<nn * K, T, k2_smem_bytes<LOGN>(), s>>>(in, in_b, M, (int)m0, pairs,
+                                                                         c->ws_dig.as<int>(), rows, out, out_b,
+                                                                         c->tb, c->tc);
+        CKL();
+        *launches += 2;
+      }
       return 0;
     }
     const size_t per = 2 * ((size_t)K * N + (size_t)ELL * N + (size_t)ELL * K * N);

@@ -164,7 +164,9 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
         },
         [&](int, int r, u32 v) { priv[pv<T>(i, r)] = (int)v; });
   }
+#ifndef EXP_NO_DCP
   dcp_private<LOGN, K, ELL>(priv, tb, cc);
+#endif
 
   const int i0 = tid << 4;
   const bool second = c + C < Cout;
@@ -184,7 +186,11 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
       ntt_fwd<LOGN>(
           ns, tb.fwd + (size_t)i * N, tc.f[i], M, [&](int jj) -> u32 { return lift(priv[pv<T>(j, jj >> SH)], q); },
           [&](int, const u32(&x)[16]) {
+#ifndef EXP_NO_MAC
             mac16(x, ra + i0, rb + i0, acc0, acc1);
+#else
+            for (int r = 0; r < 16; ++r) acc0[r] += x[r];
+#endif
           });
     }
     u32 ca[16], cb[16];
@@ -252,7 +258,9 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
           },
           [&](int, int r, u32 v) { priv[pv<T>(i, r)] = (int)v; });
     }
+#ifndef EXP_NO_DCP
     dcp_private<LOGN, K, ELL>(priv, tb, cc);
+#endif
 #pragma unroll 1
     for (int i = 0; i < K; ++i) {
       const Modulus Mi = tb.mod[i];
@@ -267,7 +275,11 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
         ntt_fwd<LOGN>(
             ns, tb.fwd + (size_t)i * N, tc.f[i], Mi, [&](int jj) -> u32 { return lift(priv[pv<T>(j, jj >> SH)], q); },
             [&](int, const u32(&x)[16]) {
-              mac16(x, ra + i0, rb + i0, acc0, acc1);
+  #ifndef EXP_NO_MAC
+            mac16(x, ra + i0, rb + i0, acc0, acc1);
+#else
+            for (int r = 0; r < 16; ++r) acc0[r] += x[r];
+#endif
             });
       }
       u32 sa[16], sb[16];

@@ -244,7 +244,9 @@ __device__ __forceinline__ void ntt_fwd(NttState& ns, const uint2* __restrict__ 
   u32* buf = ns.xbuf + ns.parity * C::N;
   ns.parity ^= 1;
   if constexpr (C::kFast) {
+#ifndef EXP_NO_FWD
     fwd_passes<LOGN, LOGN - 4>(buf, x, tid, twg, twc, q);
+#endif
 #pragma unroll
     for (int r = 0; r < 16; ++r) {  // x < (2 LOGN + 1) q: Barrett to [0, 2q), then canonical
       const u32 v = x[r] - mulhi(x[r], M.barrett) * q;

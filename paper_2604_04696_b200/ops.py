@@ -39,7 +39,9 @@ def _u32(a):
 
 
 def _mode(mode) -> int:
-    return 1 if getattr(mode, "value", mode) in ("stage", 1) else 0
+    """ExecMode / 'op' / 'stage' / 'split' -> C-ABI mode code (include/gpir.h)."""
+    v = getattr(mode, "value", mode)
+    return {"op": 0, 0: 0, "stage": 1, 1: 1, "split": 2, 2: 2}[v]
 
 
 def ntt_raw(x, basis, gadget=None):

@@ -78,13 +78,13 @@ def test_digits_extremes(G, tag):
 
 
 @pytest.mark.parametrize("tag", list(PROFILES))
-@pytest.mark.parametrize("mode", ["op", "stage"])
+@pytest.mark.parametrize("mode", ["op", "stage", "split"])
 def test_subs_and_external_product_golden(G, golden, tag, mode):
     from paper_2604_04696_b200 import ops
     _, vec = golden
     po = _po(tag)
     p = to_api(po)
-    m = G.ExecMode.STAGE_LEVEL if mode == "stage" else G.ExecMode.OPERATION_LEVEL
+    m = mode
     st, ks = vec[f"{tag}_subs_in"], vec[f"{tag}_subs_ksk"]
     out = ops.expand_stage(st, ks, po.n // 2 + 1, None, p.basis, p.gadget, m)
     assert np.array_equal(out, vec[f"{tag}_subs_out"])
@@ -92,13 +92,13 @@ def test_subs_and_external_product_golden(G, golden, tag, mode):
     assert np.array_equal(xp, vec[f"{tag}_xp_out"])
 
 
-@pytest.mark.parametrize("mode", ["op", "stage"])
+@pytest.mark.parametrize("mode", ["op", "stage", "split"])
 def test_expand_stages_and_coltor_vs_oracle(G, mode):
     from paper_2604_04696_b200 import ops
     po = O.default_params()
     p = to_api(po)
     R = po.ring
-    m = G.ExecMode.STAGE_LEVEL if mode == "stage" else G.ExecMode.OPERATION_LEVEL
+    m = mode
     rng = np.random.default_rng(99)
     uni = lambda *s: np.stack([rng.integers(0, q, size=s + (R.n,), dtype=np.uint64) for q in R.qs], axis=-2)
     B, C = 3, 4
