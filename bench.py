@@ -300,6 +300,67 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_rowshard(args, rank, world, local_rank):
+    """North-star multi-GPU mode: DB rows sharded over the ranks, queries owned
+    round-robin in blocks, NCCL all-to-all + reduce-scatter(sum) combine
+    (paper_2604_04696_b200/cluster.py).  Strong scaling: the config's DB and
+    batch are fixed and split over the ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_04696_b200 as G
+    from paper_2604_04696_b200.cluster import CudaRowShard, TorchComm, answer_row_sharded
+
+    torch.cuda.set_device(local_rank)
+    d0, d1, B, rb, pb, desc = CONFIGS[args.config]
+    if B % world or d0 % world:
+        raise SystemExit(f"batch {B} / d0 {d0} do not split over {world} ranks")
+    params = G.HeParams(G.default_basis(4096), pb)
+    d0l, b_own = d0 // world, B // world
+    rng = np.random.default_rng(500 + rank)
+    rows = rng.integers(0, 256, size=(d0l * d1, rb), dtype=np.uint8)
+    be = CudaRowShard(params, rows, d0, d1, rb, world, local_rank)
+    del rows
+    stages = G.planner.num_expand_stages(G.planner.expansion_leaves(d0, d1, params.gadget.ell))
+    evks, rgsw, queries = synthetic_material(G, params, b_own, stages, rng)
+    for b in range(b_own):
+        be.put_keys(b, evks[b], rgsw[b])
+    slots = np.arange(b_own, dtype=np.int32)
+    q = torch.from_numpy(queries.view(np.int32)).cuda()
+    comm = TorchComm() if world > 1 else type("C1", (), {"size": 1, "all_to_all": staticmethod(lambda x: x),
+                                                         "reduce_scatter_sum": staticmethod(lambda x: x[0])})()
+    step = lambda: answer_row_sharded(be, comm, q, slots, d0, d1)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        line = {
+            "metric": "PIR queries/sec (batched)", "value": B / (ms / 1e3), "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32 (mod-q, 64-bit lazy products)",
+            "data": "synthetic (random records, uniform-random key/query material)",
+            "config": {"workload": desc, "d0": d0, "d1": d1, "global_batch": B, "record_bytes": rb, "plain_bits": pb,
+                       "parallelism": f"rowshard{world} (DB rows + query owners; NCCL all-to-all + reduce-scatter)"},
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -309,6 +370,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--modes", default="", choices=["", "fused", "op"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--strategy", default="replica", choices=["replica", "rowshard"],
+                    help="multi-GPU mode: replica (DB copy + own batch per GPU) or rowshard (north-star DB row shards)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -325,6 +388,8 @@ def main():
             dist.init_process_group("gloo")
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.strategy == "rowshard":
+        run_rowshard(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
     if world > 1:

@@ -124,6 +124,24 @@ int gpir_shard_answer(gpir_ctx* ctx, const gpir_db* db, uint32_t d1_total, const
 int gpir_coltor_dev(gpir_ctx* ctx, const uint32_t* d_cts, uint32_t B, uint32_t C, const uint32_t* d_rgsw,
                     uint32_t* d_out, void* stream);
 
+/* ---- row-sharded pipeline (D0 shards + modular-add combine; north-star
+ * multi-GPU mode).  Per rank r of n (device buffers, `stream` or NULL):
+ *   1. gpir_sharded_expand: expand the rank's OWN queries (B_own) over the full
+ *      (d0, d1) tree and assemble their RGSWs; writes their row ciphertexts
+ *      d_rows[B_own][d0][2][k][n] (internal brv slot order).  The expansion and
+ *      RGSWs stay in the context for step 3.
+ *   2. (caller) all-to-all of row blocks so every rank holds all B queries'
+ *      rows of its own D0 range; gpir_sharded_rowsel multiplies them with the
+ *      local DB rows (db has d0/n rows x d1 columns) -> d_partial[B][d1][2][k][n].
+ *   3. (caller) reduce-scatter(sum, int32) of the partials by query owner;
+ *      gpir_sharded_coltor reduces the sums mod q in place and runs the
+ *      tournament for the own queries -> d_out[B_own][2][k][n] (natural order). */
+int gpir_sharded_expand(gpir_ctx* ctx, uint32_t d0, uint32_t d1, const uint32_t* d_queries, const int32_t* key_slots,
+                        uint32_t B_own, uint32_t* d_rows, void* stream);
+int gpir_sharded_rowsel(gpir_ctx* ctx, const gpir_db* db, const uint32_t* d_rows, uint32_t B, uint32_t* d_partial,
+                        void* stream);
+int gpir_sharded_coltor(gpir_ctx* ctx, uint32_t* d_sums, uint32_t B_own, uint32_t* d_out, void* stream);
+
 /* ---- operator-level parity entry points (host buffers, natural order) ---- */
 int gpir_op_ntt(gpir_ctx* ctx, const uint32_t* in, uint32_t* out, uint32_t polys, int inverse);
 int gpir_op_digits(gpir_ctx* ctx, const uint32_t* coeff, int32_t* digits_out, uint32_t polys);

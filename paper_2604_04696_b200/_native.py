@@ -53,6 +53,10 @@ _SIGS = {
                                     C.c_void_p, C.c_void_p, C.POINTER(GpirStats)]),
     "gpir_coltor_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
                                   C.c_void_p]),
+    "gpir_sharded_expand": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, _i32p, C.c_uint32, C.c_void_p,
+                                      C.c_void_p]),
+    "gpir_sharded_rowsel": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "gpir_sharded_coltor": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
     "gpir_op_ntt": (C.c_int, [C.c_void_p, _u32p, _u32p, C.c_uint32, C.c_int]),
     "gpir_op_digits": (C.c_int, [C.c_void_p, _u32p, _i32p, C.c_uint32]),
     "gpir_op_expand_stage": (C.c_int, [C.c_void_p, _u32p, C.c_uint32, C.c_uint32, _u32p, C.c_uint32, C.c_int, _u32p]),

@@ -105,6 +105,9 @@ struct gpir_ctx {
   DevBuf ws_coeff, ws_dig, ws_dn, ws_io0, ws_io1, ws_a8;
   int rowsel_engine = 0;  // 0 auto, 1 CUDA cores, 2 tensor cores
   int num_sms = 148;
+  // row-sharded session state (gpir_sharded_expand -> gpir_sharded_coltor)
+  u32* sh_leaves = nullptr;
+  uint32_t sh_B = 0, sh_d0 = 0, sh_d1 = 0, sh_total = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[12];
   std::mutex mu;
@@ -661,6 +664,65 @@ struct Engine {
     return 0;
   }
 
+  // ---- row-sharded pipeline (D0 shards, modular-add combine) -----------------------
+  // expand the rank's own queries over the full (d0, d1) tree, assemble their
+  // RGSWs, and export the row leaves (B, d0, ct) in the internal brv layout.
+  static int sh_expand(gpir_ctx* c, uint32_t d0, uint32_t d1, const u32* d_q, const int32_t* slots, int B,
+                       u32* d_rows, cudaStream_t s) {
+    const uint32_t total = leaves_of(d0, d1, ELL), bits = ilog2(d1);
+    int rc;
+    if ((rc = check_keys(c, slots, B, stages_of(total), bits > 0))) return rc;
+    if ((rc = ensure_ws(c, B, total, d1, bits))) return rc;
+    CK(cudaMemcpyAsync(c->ws_kslot.p, slots, (size_t)B * 4, cudaMemcpyHostToDevice, s));
+    if ((rc = bitrev_rows(c, d_q, c->ws_state0.as<u32>(), (size_t)B * 2 * K, s))) return rc;
+    uint32_t launches = 0;
+    u32* leaves = nullptr;
+    if ((rc = expand_all(c, B, total, nullptr, 0, c->ws_kslot.as<int>(), &leaves, s, &launches))) return rc;
+    if (bits > 0) {
+      const int M = (int)(bits * ELL);
+      if ((rc = ext_product(c, leaves + (size_t)d0 * CT, total, B, M, 0, c->ws_arows.as<u32>(), (size_t)M,
+                            skrgsw_rows(c, c->ws_kslot.as<int>()), default_mode((size_t)B * M), s, &launches)))
+        return rc;
+    }
+    CK(cudaMemcpy2DAsync(d_rows, (size_t)d0 * CT * 4, leaves, (size_t)total * CT * 4, (size_t)d0 * CT * 4, B,
+                         cudaMemcpyDeviceToDevice, s));
+    c->sh_leaves = leaves;
+    c->sh_B = B;
+    c->sh_d0 = d0;
+    c->sh_d1 = d1;
+    c->sh_total = total;
+    return 0;
+  }
+
+  // ColTor for the session's own queries from combined RowSel sums (int32,
+  // brv, sum of shard partials < n q): reduce mod q, run all log2(d1) stages.
+  static int sh_coltor(gpir_ctx* c, u32* d_sums, int B, u32* d_out, cudaStream_t s) {
+    if (!c->sh_leaves || (uint32_t)B != c->sh_B) FAIL(GPIR_INVALID_STATE, "gpir_sharded_expand must precede gpir_sharded_coltor");
+    const uint32_t d1 = c->sh_d1, bits = ilog2(d1), total = c->sh_total, d0 = c->sh_d0;
+    const size_t rows = (size_t)B * d1 * 2 * K;
+    k_mod_rows<<<(unsigned)((rows * N + 255) / 256), 256, 0, s>>>(d_sums, rows, LOGN, K, c->tb);
+    CKL();
+    u32* cur = d_sums;
+    u32* bufs[2] = {c->ws_ct0.as<u32>(), c->ws_ct1.as<u32>()};
+    uint32_t launches = 0;
+    int rc;
+    for (uint32_t j = 0; j < bits; ++j) {
+      const int C = (int)(d1 >> j);
+      RowsDesc r;
+      r.lo = c->ws_arows.as<u32>() + (size_t)j * ELL * CT;
+      r.lo_b = (size_t)bits * ELL * CT;
+      r.hi = c->sh_leaves + (size_t)(d0 + j * ELL) * CT;
+      r.hi_b = (size_t)total * CT;
+      r.slot = nullptr;
+      u32* dst = bufs[j & 1];
+      if ((rc = ext_product(c, cur, (size_t)C, B, C / 2, 1, dst, (size_t)C / 2, r, default_mode((size_t)B * C / 2), s,
+                            &launches)))
+        return rc;
+      cur = dst;
+    }
+    return bitrev_rows(c, cur, d_out, (size_t)B * 2 * K, s);
+  }
+
   static int coltor_dev(gpir_ctx* c, const u32* d_cts, int B, int C, const u32* d_rgsw, u32* d_out, cudaStream_t s) {
     const uint32_t bits = ilog2((uint32_t)C);
     int rc;
@@ -1201,6 +1263,68 @@ int gpir_shard_answer(gpir_ctx* c, const gpir_db* db, uint32_t d1_total, const u
   int rc;
   switch (c->logn * 10000 + c->k * 100 + c->ell) {
     GPIR_COMBOS(DISPATCH_CASE_SHARD)
+    default:
+      FAIL(GPIR_UNSUPPORTED, "unsupported combination");
+  }
+  if (rc) return rc;
+  if (!stream) CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+#define DISPATCH_CASE_SHX(L, K_, E) \
+  case L * 10000 + K_ * 100 + E:    \
+    rc = Engine<L, K_, E>::sh_expand(c, d0, d1, d_queries, key_slots, (int)B, d_rows, s); break;
+
+int gpir_sharded_expand(gpir_ctx* c, uint32_t d0, uint32_t d1, const uint32_t* d_queries, const int32_t* key_slots,
+                        uint32_t B, uint32_t* d_rows, void* stream) {
+  if (!c || !d_queries || !key_slots || !d_rows || !B || !d0 || !d1 || (d1 & (d1 - 1)))
+    FAIL(GPIR_INVALID_ARGUMENT, "invalid sharded expansion input");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  int rc;
+  switch (c->logn * 10000 + c->k * 100 + c->ell) {
+    GPIR_COMBOS(DISPATCH_CASE_SHX)
+    default:
+      FAIL(GPIR_UNSUPPORTED, "unsupported combination");
+  }
+  if (rc) return rc;
+  if (!stream) CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int gpir_sharded_rowsel(gpir_ctx* c, const gpir_db* db, const uint32_t* d_rows, uint32_t B, uint32_t* d_partial,
+                        void* stream) {
+  if (!c || !db || !d_rows || !d_partial || !B) FAIL(GPIR_INVALID_ARGUMENT, "invalid sharded rowsel input");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  int rc;
+  uint32_t launches = 0;
+  gpir_db* mdb = const_cast<gpir_db*>(db);
+  switch (c->logn * 10000 + c->k * 100 + c->ell) {
+    case 120405: rc = Engine<12, 4, 5>::rowsel(c, d_rows, (size_t)db->d0 * c->ct_words(), (int)B, mdb, d_partial, s, &launches); break;
+    case 80205: rc = Engine<8, 2, 5>::rowsel(c, d_rows, (size_t)db->d0 * c->ct_words(), (int)B, mdb, d_partial, s, &launches); break;
+    case 60206: rc = Engine<6, 2, 6>::rowsel(c, d_rows, (size_t)db->d0 * c->ct_words(), (int)B, mdb, d_partial, s, &launches); break;
+    default: FAIL(GPIR_UNSUPPORTED, "unsupported combination");
+  }
+  if (rc) return rc;
+  if (!stream) CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+#define DISPATCH_CASE_SHC(L, K_, E) \
+  case L * 10000 + K_ * 100 + E:    \
+    rc = Engine<L, K_, E>::sh_coltor(c, d_sums, (int)B, d_out, s); break;
+
+int gpir_sharded_coltor(gpir_ctx* c, uint32_t* d_sums, uint32_t B, uint32_t* d_out, void* stream) {
+  if (!c || !d_sums || !d_out || !B) FAIL(GPIR_INVALID_ARGUMENT, "invalid sharded coltor input");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  int rc;
+  switch (c->logn * 10000 + c->k * 100 + c->ell) {
+    GPIR_COMBOS(DISPATCH_CASE_SHC)
     default:
       FAIL(GPIR_UNSUPPORTED, "unsupported combination");
   }

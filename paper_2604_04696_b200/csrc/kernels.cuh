@@ -628,6 +628,16 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
       [&](int i0, const u32(&x)[16]) { st16(dst + i0, x); });
 }
 
+// In-place reduction of limb rows holding sums of up to 16 canonical residues
+// (the NCCL modular-add combine of row-sharded RowSel partials).
+__global__ void k_mod_rows(u32* __restrict__ x, size_t rows, int logn, int k, Tables tb) {
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (rows << logn)) return;
+  const int limb = (int)((g >> logn) % k);
+  const Modulus& M = tb.mod[limb];
+  x[g] = x[g] % M.q;
+}
+
 // Bit-reversal permutation of whole limb rows (natural <-> brv; an involution).
 __global__ void k_bitrev_rows(const u32* __restrict__ in, u32* __restrict__ out, size_t rows, int logn) {
   const size_t n = (size_t)1 << logn;

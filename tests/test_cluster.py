@@ -1,0 +1,181 @@
+"""Row-sharded multi-rank serving (paper_2604_04696_b200.cluster).
+
+CPU: world_size-2 gloo processes run the real orchestration and NCCL-style
+collectives with the oracle as the per-rank compute backend; the combined
+responses must equal the single-process pipeline bit for bit.
+GPU: two virtual ranks on one device (threads + an in-process transport)
+drive the real C-ABI sharded kernels; responses must equal the oracle's."""
+import os
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import gpir_oracle as O
+
+D0, D1, RB = 8, 4, 32
+
+
+class OracleRowShard:
+    """Oracle compute for one rank (tests only)."""
+
+    def __init__(self, po, db_pm_local, d0, d1, clients_own):
+        self.po, self.db, self.d0, self.d1 = po, db_pm_local, d0, d1
+        self.clients = clients_own
+        R = po.ring
+        self.ct = 2 * R.k * R.n
+
+    def swap01(self, x):
+        return x.transpose(0, 1).contiguous()
+
+    def expand(self, q_own, _slots):
+        R = self.po.ring
+        qs = q_own.numpy().astype(np.uint64).reshape(-1, 2, R.k, R.n)
+        evks = np.stack([c.evks for c in self.clients])
+        leaves = O.expand(qs, evks, self.d0, self.d1, self.po)
+        self.leaves = leaves
+        return torch.from_numpy(leaves[:, :self.d0].reshape(len(qs), self.d0, self.ct).astype(np.int64))
+
+    def rowsel(self, rows_all):
+        R = self.po.ring
+        rows = rows_all.numpy().astype(np.uint64).reshape(rows_all.shape[0], -1, 2, R.k, R.n)
+        sel = O.rowsel(rows, self.db, R)
+        return torch.from_numpy(sel.reshape(sel.shape[0], self.d1, self.ct).astype(np.int64))
+
+    def coltor(self, sums):
+        R = self.po.ring
+        sel = sums.numpy().astype(np.uint64).reshape(sums.shape[0], self.d1, 2, R.k, R.n) % R.q
+        rg = O.build_rgsw(self.leaves[:, self.d0:], np.stack([c.sk_rgsw for c in self.clients]), self.po)
+        out = O.coltor(sel, rg, self.po)
+        return torch.from_numpy(out.reshape(out.shape[0], self.ct).astype(np.int64))
+
+
+def _material(po, n_queries, seed=3):
+    rng = np.random.default_rng(seed)
+    recs = [rng.integers(0, 256, size=RB, dtype=np.uint8).tobytes() for _ in range(D0 * D1)]
+    clients = [O.client_keygen(po, D0, D1, rng) for _ in range(n_queries)]
+    targets = [(int(rng.integers(0, D0)), int(rng.integers(0, D1))) for _ in range(n_queries)]
+    qs = [O.client_query(c, i, j, D0, D1, rng) for c, (i, j) in zip(clients, targets)]
+    return recs, clients, targets, np.stack(qs)
+
+
+def _rank_main(rank, world, port, out_path):
+    import torch.distributed as dist
+
+    from paper_2604_04696_b200.cluster import TorchComm, answer_row_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    po = O.test_params()
+    B = 2 * world
+    recs, clients, _, qs = _material(po, B)
+    db = O.encode_database(recs, D0, D1, RB, po)               # (d1, d0, kn)
+    d0l = D0 // world
+    db_local = np.ascontiguousarray(db[:, rank * d0l:(rank + 1) * d0l])
+    own = slice(rank * B // world, (rank + 1) * B // world)
+    be = OracleRowShard(po, db_local, D0, D1, clients[own])
+    q_own = torch.from_numpy(qs[own].astype(np.int64))
+    out = answer_row_sharded(be, TorchComm(), q_own, None, D0, D1)
+    np.save(out_path + f".{rank}.npy", out.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_row_sharded_gloo_matches_single_process(tmp_path):
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world = 2
+    path = str(tmp_path / "resp")
+    mp.start_processes(_rank_main, args=(world, port, path), nprocs=world, start_method="spawn", join=True)
+    got = np.concatenate([np.load(path + f".{r}.npy") for r in range(world)]).astype(np.uint64)
+    po = O.test_params()
+    B = 2 * world
+    recs, clients, targets, qs = _material(po, B)
+    db = O.encode_database(recs, D0, D1, RB, po)
+    want = O.answer_batch(qs, np.stack([c.evks for c in clients]), np.stack([c.sk_rgsw for c in clients]), db,
+                          D0, D1, po)
+    R = po.ring
+    assert np.array_equal(got.reshape(want.shape), want)
+    for c, (i, j), ct in zip(clients, targets, want):
+        assert O.decode_plain(O.decrypt(c, ct), RB, po) == recs[i * D1 + j]
+
+
+class _ThreadComm:
+    """In-process transport for n threads (one per virtual rank)."""
+
+    def __init__(self, n):
+        self.n = n
+        self.bar = threading.Barrier(n)
+        self.slots = [None] * n
+
+    def view(self, rank):
+        outer = self
+
+        class V:
+            size = outer.n
+
+            def all_to_all(self, send):
+                outer.slots[rank] = send
+                outer.bar.wait()
+                recv = torch.stack([outer.slots[s][rank] for s in range(outer.n)])
+                outer.bar.wait()
+                return recv
+
+            def reduce_scatter_sum(self, x):
+                outer.slots[rank] = x
+                outer.bar.wait()
+                out = sum(outer.slots[s][rank] for s in range(outer.n))
+                outer.bar.wait()
+                return out
+
+        return V()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_row_sharded_gpu_virtual_ranks(world):
+    from paper_2604_04696_b200.cluster import CudaRowShard, answer_row_sharded
+    from tests.helpers import to_api
+
+    po = O.default_params(plain_bits=16)
+    p = to_api(po)
+    d0, d1, rb = 16, 8, 1024
+    B = 2 * world
+    rng = np.random.default_rng(77)
+    recs = rng.integers(0, 256, size=(d0 * d1, rb), dtype=np.uint8)
+    clients = [O.client_keygen(po, d0, d1, rng) for _ in range(B)]
+    targets = [(int(rng.integers(0, d0)), int(rng.integers(0, d1))) for _ in range(B)]
+    qs = np.stack([O.client_query(c, i, j, d0, d1, rng) for c, (i, j) in zip(clients, targets)])
+    comm = _ThreadComm(world)
+    d0l = d0 // world
+    bes, outs = [], [None] * world
+    for r in range(world):
+        be = CudaRowShard(p, recs[r * d0l * d1:(r + 1) * d0l * d1], d0, d1, rb, world, 0)
+        own = range(r * B // world, (r + 1) * B // world)
+        for s, b in enumerate(own):
+            be.put_keys(s, clients[b].evks, clients[b].sk_rgsw)
+        bes.append(be)
+
+    def run(r):
+        own = slice(r * B // world, (r + 1) * B // world)
+        q = torch.from_numpy(qs[own].astype(np.uint32).view(np.int32)).cuda()
+        slots = np.arange(B // world, dtype=np.int32)
+        outs[r] = answer_row_sharded(bes[r], comm.view(r), q, slots, d0, d1).cpu().numpy().view(np.uint32)
+        torch.cuda.synchronize()
+
+    ths = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    got = np.concatenate(outs).astype(np.uint64).reshape(B, 2, po.ring.k, po.n)
+    db = O.encode_database([r.tobytes() for r in recs], d0, d1, rb, po)
+    want = O.answer_batch(qs, np.stack([c.evks for c in clients]), np.stack([c.sk_rgsw for c in clients]), db,
+                          d0, d1, po)
+    assert np.array_equal(got, want)
