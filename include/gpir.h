@@ -69,7 +69,7 @@ gpir_ctx* gpir_ctx_create(int device, uint32_t n, uint32_t k, const uint32_t* q,
                           uint32_t z_bits, uint32_t ell);
 void gpir_ctx_destroy(gpir_ctx* ctx);
 int gpir_ctx_device(const gpir_ctx* ctx);
-/* RowSel engine: 0 = auto (tensor cores when 2B <= 128 and d0 <= 1024),
+/* RowSel engine: 0 = auto (tensor cores when d0 <= 1024; A tiles of 128 rows),
  * 1 = CUDA cores (64-bit lazy IMAD), 2 = tensor cores (tcgen05 kind::i8). */
 int gpir_set_rowsel_engine(gpir_ctx* ctx, int engine);
 /* Supported (log2 n, k, ell) combinations are compiled in; 1 if supported. */

@@ -385,7 +385,7 @@ struct Engine {
   static bool tc_eligible(gpir_ctx* c, int B, const gpir_db* db) {
     const int KN = K * N;
     if (c->rowsel_engine == 1) return false;
-    return 2 * B <= 128 && db->d0 <= 1024 && KN % PK_P == 0;
+    return db->d0 <= 1024 && KN % PK_P == 0;
   }
 
   // RowSel: tensor-core path (byte-plane u8 GEMMs, rowsel_tc.cuh) when the
@@ -397,8 +397,11 @@ struct Engine {
     int rc;
     if (tc_eligible(c, B, db)) {
       const int M = 2 * B;
-      const bool m64 = M <= 64;
+      const int RA = M <= 128 ? M : 128;  // rows per A tile
+      const int mtiles = (M + RA - 1) / RA;
+      const bool m64 = RA <= 64;
       const int NT = (m64 && db->d1 >= 64) ? 64 : 32;  // two TMEM accumulator buffers either way
+      const int PST = m64 ? 8 : 4;                     // p per staged epilogue flush
       const int nchunks = ((int)db->d0 + TC_KC - 1) / TC_KC;
       const int ntiles = ((int)db->d1 + NT - 1) / NT;
       if (db->d8_nt != NT) {
@@ -410,10 +413,10 @@ struct Engine {
         CKL();
         db->d8_nt = NT;
       }
-      if ((rc = c->ws_a8.ensure((size_t)KN * nchunks * 4 * M * TC_KC))) return rc;
+      if ((rc = c->ws_a8.ensure((size_t)KN * nchunks * mtiles * 4 * RA * TC_KC))) return rc;
       PackSrc pa{leaves, a_b_words, (size_t)KN, 2, 2 * (size_t)KN};
-      dim3 g(KN / PK_P, (M + PK_R - 1) / PK_R, nchunks * (TC_KC / PK_K));
-      k_pack_planes<<<g, 256, 0, s>>>(pa, M, (int)db->d0, M, 1, nchunks, c->ws_a8.as<uint8_t>());
+      dim3 g(KN / PK_P, (mtiles * RA + PK_R - 1) / PK_R, nchunks * (TC_KC / PK_K));
+      k_pack_planes<<<g, 256, 0, s>>>(pa, M, (int)db->d0, RA, mtiles, nchunks, c->ws_a8.as<uint8_t>());
       CKL();
       if (ev_mid) CK(cudaEventRecord(ev_mid, s));
       TcArgs ta;
@@ -421,18 +424,20 @@ struct Engine {
       ta.D8 = db->d8.as<uint8_t>();
       ta.out = sel;
       ta.M = M;
+      ta.RA = RA;
+      ta.mtiles = mtiles;
       ta.d1 = (int)db->d1;
       ta.ntiles = ntiles;
       ta.nchunks = nchunks;
       ta.KN = KN;
       ta.logn = LOGN;
-      ta.items = KN * ntiles;
-      const uint32_t stage_bytes = ((4u * M * TC_KC + 4u * NT * TC_KC) + 127u) & ~127u;
-      const size_t outbuf = (size_t)TC_PST * M * (NT + 1) * 4;
+      ta.items = KN * ntiles * mtiles;
+      const uint32_t stage_bytes = ((4u * RA * TC_KC + 4u * NT * TC_KC) + 127u) & ~127u;
+      const size_t outbuf = (size_t)PST * RA * (NT + 1) * 4;
       const size_t fixed = 4096 + outbuf + 2 * TC_MAX_STAGES * 8 + 4 * 8 + 16;
       ta.stages = std::max(2, std::min<int>(TC_MAX_STAGES, (int)((220u * 1024u - fixed) / stage_bytes)));
       const size_t smem = (size_t)ta.stages * stage_bytes + fixed;
-      const int grid = std::min(KN / TC_PST, c->num_sms);
+      const int grid = std::min(KN / PST, c->num_sms);
       static const bool prof_on = getenv("GPIR_TC_PROF") != nullptr;
       DevBuf profbuf;
       ta.prof = nullptr;
@@ -441,7 +446,8 @@ struct Engine {
         CK(cudaMemsetAsync(profbuf.p, 0, profbuf.bytes, s));
         ta.prof = profbuf.as<unsigned long long>();
       }
-      auto kern = NT == 64 ? k_rowsel_tc<64, true> : (m64 ? k_rowsel_tc<32, true> : k_rowsel_tc<32, false>);
+      auto kern = NT == 64 ? k_rowsel_tc<64, true, 8>
+                           : (m64 ? k_rowsel_tc<32, true, 8> : k_rowsel_tc<32, false, 4>);
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<grid, TC_THREADS, smem, s>>>(ta, c->tb);
       CKL();

@@ -13,7 +13,7 @@
 // Operands are pre-packed in HBM in the UMMA canonical K-major no-swizzle
 // layout, one contiguous block per (p, 64-byte K chunk) so each pipeline
 // stage is two cp.async.bulk copies (UBLKCP):
-//   A8[p][c][plane][g][row m][16 B]          (rows = 2B, packed per batch)
+//   A8[p][c][mtile][plane][g][row][16 B]     (rows = 2B in tiles of <= 128, per batch)
 //   D8[p][c][ntile][plane][g][row 32][16 B]  (rows = DB columns, packed once)
 // Work item = (p, NT-column tile, NT = 32 or 64); a persistent CTA per SM runs a multi-stage
 // TMA->MMA pipeline (warp 0 producer, warp 1 single-thread MMA issuer,
@@ -136,7 +136,7 @@ __device__ __forceinline__ size_t pack_src_off(const PackSrc& s, int r) {
 constexpr int PK_P = 128, PK_R = 4, PK_K = 16;
 __global__ void __launch_bounds__(256)
     k_pack_planes(PackSrc src, int R, int Kd, int RT, int ntiles, int nchunks, uint8_t* __restrict__ dst) {
-  __shared__ u32 tile[PK_R][PK_K][PK_P + 1];
+  __shared__ __align__(16) u32 tile[PK_R][PK_K][PK_P];
   const int p0 = blockIdx.x * PK_P;
   const int r0 = blockIdx.y * PK_R;
   const int kg = blockIdx.z;  // global 16-byte K group
@@ -156,11 +156,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int run = warp + 8 * i;
-    u32* t = &tile[run / PK_K][run % PK_K][lane * 4];
-    t[0] = vals[i].x;
-    t[1] = vals[i].y;
-    t[2] = vals[i].z;
-    t[3] = vals[i].w;
+    *reinterpret_cast<uint4*>(&tile[run / PK_K][run % PK_K][lane * 4]) = vals[i];  // conflict-free 128-bit
   }
   __syncthreads();
   const int pp = tid & (PK_P - 1);
@@ -197,54 +193,54 @@ struct TcArgs {
   const uint8_t* A8;  // [p][c][plane][g][M][16]
   const uint8_t* D8;  // [p][c][nt][plane][g][32][16]
   u32* out;           // (B, d1, 2, KN) standard layout
-  int M;              // 2B rows (<= 128)
+  int M;              // 2B rows (any; tiled by RA)
+  int RA, mtiles;     // rows per A tile (<= 128) and A tiles
   int d1, ntiles, nchunks, KN, logn;
   int items;          // KN * ntiles
   int stages;         // pipeline depth (<= TC_MAX_STAGES)
   unsigned long long* prof;  // optional per-CTA cycle counters [grid][8] (GPIR_TC_PROF)
 };
 
-// CTA-local work order: blocks of TC_PST consecutive p (round-robin over
-// CTAs), each block swept over all column tiles, TC_PST items per sweep, so
-// the epilogue can stage TC_PST consecutive p in shared memory and write
-// full 32-byte sectors of the p-innermost output.
-constexpr int TC_PST = 8;
+// CTA-local work order: blocks of PST consecutive p (round-robin over CTAs),
+// each block swept over all (row tile, column tile) pairs, PST items per
+// sweep, so the epilogue can stage PST consecutive p in shared memory and
+// write full sectors of the p-innermost output.
+template <int PST>
 struct TcSched {
-  int blk, nt, j;
-  __device__ __forceinline__ TcSched() : blk(blockIdx.x), nt(0), j(0) {}
-  __device__ __forceinline__ bool valid(const TcArgs& a) const { return blk * TC_PST < a.KN; }
-  __device__ __forceinline__ int p() const { return blk * TC_PST + j; }
+  int blk, mt, nt, j;
+  __device__ __forceinline__ TcSched() : blk(blockIdx.x), mt(0), nt(0), j(0) {}
+  __device__ __forceinline__ bool valid(const TcArgs& a) const { return blk * PST < a.KN; }
+  __device__ __forceinline__ int p() const { return blk * PST + j; }
   __device__ __forceinline__ void next(const TcArgs& a) {
-    if (++j == TC_PST) {
+    if (++j == PST) {
       j = 0;
       if (++nt == a.ntiles) {
         nt = 0;
-        blk += gridDim.x;
+        if (++mt == a.mtiles) {
+          mt = 0;
+          blk += gridDim.x;
+        }
       }
     }
   }
 };
 
-// TC_NT: DB columns per work item (= MMA N).  M64: 2B <= 64 uses the M=64
-// MMA shape, whose accumulator rows occupy lanes 0-15 of each TMEM lane
-// quarter, so the two accumulator buffers interleave at lane offsets 0 / 16
-// (same columns) and every epilogue warp owns 16 rows; otherwise M=128 with
-// buffers side by side in columns when 2 * 7 * NT <= 512.
-template <int TC_NT, bool M64>
+template <int TC_NT, bool M64, int TC_PST>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb) {
+  using Sched = TcSched<TC_PST>;
   constexpr int TC_ACC_COLS = 7 * TC_NT;
   constexpr int NBUF = (M64 || 2 * TC_ACC_COLS <= 512) ? 2 : 1;
   static_assert(TC_ACC_COLS <= 512, "accumulators exceed TMEM");
   extern __shared__ __align__(1024) uint8_t tc_smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t bytesA = 4u * a.M * TC_KC;
+  const uint32_t bytesA = 4u * a.RA * TC_KC;
   const uint32_t bytesD = 4u * TC_NT * TC_KC;
   const uint32_t stage_bytes = (bytesA + bytesD + 127u) & ~127u;
   uint8_t* stages = tc_smem;
   const int NS = a.stages;
   u32* outbuf = reinterpret_cast<u32*>(tc_smem + NS * stage_bytes + 4096);  // after the MMA over-read pad
   const int OB_ROW = TC_NT + 1;  // padded row: conflict-free column writes
-  uint64_t* full = reinterpret_cast<uint64_t*>(outbuf + TC_PST * a.M * OB_ROW);
+  uint64_t* full = reinterpret_cast<uint64_t*>(outbuf + TC_PST * a.RA * OB_ROW);
   uint64_t* empty = full + TC_MAX_STAGES;
   uint64_t* tfull = empty + TC_MAX_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -274,14 +270,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
   if (warp == 0) {  // producer: whole warp walks the schedule, one lane issues the bulk copies
     int s = 0;
     uint32_t ph = 0;
-    for (TcSched sc; sc.valid(a); sc.next(a)) {
+    for (Sched sc; sc.valid(a); sc.next(a)) {
       const int p = sc.p(), nt = sc.nt;
       for (int c = 0; c < a.nchunks; ++c) {
         mbar_wait(&empty[s], ph ^ 1);
         if (elect_one()) {
           uint8_t* sa = stages + s * stage_bytes;
           mbar_expect_tx(&full[s], bytesA + bytesD);
-          bulk_g2s(sa, a.A8 + ((size_t)p * a.nchunks + c) * bytesA, bytesA, &full[s]);
+          bulk_g2s(sa, a.A8 + (((size_t)p * a.nchunks + c) * a.mtiles + sc.mt) * bytesA, bytesA, &full[s]);
           bulk_g2s(sa + bytesA, a.D8 + (((size_t)p * a.nchunks + c) * a.ntiles + nt) * bytesD, bytesD, &full[s]);
         }
         __syncwarp();
@@ -296,9 +292,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
     int s = 0;
     uint32_t ph = 0;
     int local = 0;
-    const uint32_t a_ks = (2u * a.M * 16u) >> 4;         // descriptor step of one 32-byte K step
-    const uint32_t a_pl = (uint32_t)(a.M * TC_KC) >> 4;  // ... of one byte plane
-    for (TcSched sc; sc.valid(a); sc.next(a), ++local) {
+    const uint32_t a_ks = (2u * a.RA * 16u) >> 4;         // descriptor step of one 32-byte K step
+    const uint32_t a_pl = (uint32_t)(a.RA * TC_KC) >> 4;  // ... of one byte plane
+    for (Sched sc; sc.valid(a); sc.next(a), ++local) {
       const int ab = (NBUF == 2) ? (local & 1) : 0;
       const uint32_t aph = (NBUF == 2) ? ((local >> 1) & 1) : (local & 1);
       long long t0 = clock64();
@@ -315,7 +311,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sa = smem_u32(stages + s * stage_bytes);
-          const uint64_t a0 = umma_desc(sa, a.M * 16, 128);
+          const uint64_t a0 = umma_desc(sa, a.RA * 16, 128);
           const uint64_t b0 = umma_desc(sa + bytesA, TC_NT * 16, 128);
 #pragma unroll
           for (int ks = 0; ks < TC_KC / 32; ++ks) {
@@ -346,7 +342,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
     const int quad = warp & 3;
     const int etid = (warp - 2) * 32 + lane;  // 0..127
     int local = 0;
-    for (TcSched sc; sc.valid(a); sc.next(a), ++local) {
+    for (Sched sc; sc.valid(a); sc.next(a), ++local) {
       const int ab = (NBUF == 2) ? (local & 1) : 0;
       const uint32_t aph = (NBUF == 2) ? ((local >> 1) & 1) : (local & 1);
       const int p = sc.p(), nt = sc.nt;
@@ -355,21 +351,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
       long long e1 = clock64();
       if (a.prof && lane == 0 && quad == 0) a.prof[blockIdx.x * 8 + 3] += e1 - e0;  // epilogue waits
       tc_fence_after();
-      // row held by this thread's TMEM lane for accumulator buffer ab
-      const int m = M64 ? quad * 16 + (lane & 15) : quad * 32 + lane;
+      // tile row held by this thread's TMEM lane for accumulator buffer ab
+      const int ml = M64 ? quad * 16 + (lane & 15) : quad * 32 + lane;
+      const int m = sc.mt * a.RA + ml;
       const bool mine = M64 ? ((lane >> 4) == ab) : true;
-      if ((M64 ? quad * 16 : quad * 32) < a.M) {
+      if ((M64 ? quad * 16 : quad * 32) < a.RA) {
         const Modulus M = tb.mod[p >> a.logn];
         const uint32_t tl = M64 ? tbase + ((uint32_t)(quad * 32) << 16)
                                 : tbase + ((uint32_t)(quad * 32) << 16) + ab * TC_ACC_COLS;
-        u32* orow = outbuf + ((size_t)sc.j * a.M + m) * OB_ROW;
+        u32* orow = outbuf + ((size_t)sc.j * a.RA + ml) * OB_ROW;
 #pragma unroll 1
         for (int c8 = 0; c8 < TC_NT; c8 += 8) {
           uint32_t v[7][8];
 #pragma unroll
           for (int u = 0; u < 7; ++u) tmem_ld8(tl + u * TC_NT + c8, v[u]);
           tmem_ld_wait();
-          if (mine && m < a.M) {
+          if (mine && ml < a.RA && m < a.M) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               u64 acc = 0;
@@ -386,16 +383,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
       if (sc.j == TC_PST - 1) {                 // flush TC_PST consecutive p as 32-byte runs
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const int p0 = sc.blk * TC_PST;
-        for (int w = etid; w < a.M * TC_NT; w += 128) {
-          const int mm = w / TC_NT, cc = w % TC_NT;
+        for (int w = etid; w < a.RA * TC_NT; w += 128) {
+          const int ml = w / TC_NT, cc = w % TC_NT;
+          const int mm = sc.mt * a.RA + ml;
           const int n = nt * TC_NT + cc;
-          if (n < a.d1) {
+          if (n < a.d1 && mm < a.M) {
             u32 o[TC_PST];
 #pragma unroll
-            for (int j = 0; j < TC_PST; ++j) o[j] = outbuf[((size_t)j * a.M + mm) * OB_ROW + cc];
+            for (int j = 0; j < TC_PST; ++j) o[j] = outbuf[((size_t)j * a.RA + ml) * OB_ROW + cc];
             uint4* dst = reinterpret_cast<uint4*>(a.out + (((size_t)(mm >> 1) * a.d1 + n) * 2 + (mm & 1)) * a.KN + p0);
-            dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-            dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+#pragma unroll
+            for (int v = 0; v < TC_PST / 4; ++v) dst[v] = make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
           }
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");

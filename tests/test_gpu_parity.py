@@ -133,9 +133,9 @@ def test_rowsel_golden(G, golden, tag):
 
 
 @pytest.mark.parametrize("engine", ["cudacore", "tensorcore"])
-@pytest.mark.parametrize("shape", [(1, 5, 2), (3, 64, 16), (32, 70, 64), (64, 256, 128), (17, 129, 1)])
+@pytest.mark.parametrize("shape", [(1, 5, 2), (3, 64, 16), (32, 70, 64), (64, 256, 128), (17, 129, 1), (65, 64, 32), (128, 130, 64)])
 def test_rowsel_engines_vs_oracle(G, engine, shape):
-    """Both RowSel engines, ragged shapes (B, d0, d1) incl. M = 2B = 128, d0 not a
+    """Both RowSel engines, ragged shapes (B, d0, d1) incl. M = 2B = 128 and > 128 (row tiles), d0 not a
     multiple of the 64-byte K chunk, d1 below and above the 32-column tile,
     and residues at q-1 (largest byte planes)."""
     from types import SimpleNamespace
