@@ -20,7 +20,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -49,56 +48,63 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons sampled (NVML, every 5 ms) during the timed region."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.out = []
+        self.sm, self.mx, self.reasons = [], None, set()
+        self._stop = threading.Event()
+        self.t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def loop():
+                while True:
+                    self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.reasons.update(k for k, m in self.REASONS.items() if r & m)
+                    if self._stop.wait(0.005):
+                        return
+
+            self.t = threading.Thread(target=loop, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # no NVML: report the gap instead of a number
+            self.err = str(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.out.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.t is not None:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], 0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.out:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[2:6]):
-                if v.lower() in ("active", "1", "yes"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
+
+
+def ncu_traffic(prefix="k_rowsel_tc"):
+    """dram read+write bytes per launch of the RowSel kernel from the newest committed
+    `ncu --set full` summary (profiles/*_ncu.json, tools/ncu_summary.py), or None."""
+    import glob
+
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu.json")), key=os.path.getmtime):
+        try:
+            js = json.load(open(f))
+        except Exception:
+            continue
+        for k, d in js.get("kernels", {}).items():
+            if k.startswith(prefix) and "traffic_bytes" in d:
+                best = (d["traffic_bytes"], os.path.basename(f), k)
+    return best
 
 
 def synthetic_material(G, params, B, stages, rng):
@@ -153,6 +159,7 @@ def run_reference(args, rank, world):
         return
     d0, d1, B, rb, pb, desc = CONFIGS[args.config]
     qps, sec, cores, sample = cpu_reference(args.config, args.steps)
+    tr = ncu_traffic()
     line = {
         "metric": "PIR queries/sec (batched)", "value": qps, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
@@ -214,12 +221,13 @@ def run_ours(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
     # phase breakdown + RowSel kernel duration, CUDA events on the launch stream (untimed pass)
-    ph = {"ExpandQuery": [], "RgswAssembly": [], "RowSel": [], "ColTor": [], "total": []}
+    ph = {"ExpandQuery": [], "RgswAssembly": [], "RowSelPack": [], "RowSel": [], "ColTor": [], "total": []}
     launches = 0
     for _ in range(max(1, min(args.steps, 5))):
         step(st)
         ph["ExpandQuery"].append(st.ms_expand)
         ph["RgswAssembly"].append(st.ms_rgsw)
+        ph["RowSelPack"].append(st.ms_rowsel - st.ms_rowsel_kernel)
         ph["RowSel"].append(st.ms_rowsel_kernel)
         ph["ColTor"].append(st.ms_coltor)
         ph["total"].append(st.ms_total)
@@ -274,6 +282,7 @@ def run_ours(args, rank, world, local_rank):
     rs_bytes = d0 * d1 * KN * 4 + B * d0 * 2 * KN * 4 + B * d1 * 2 * KN * 4
     rs_ms = float(np.mean(ph["RowSel"]))
     achieved = rs_bytes / (rs_ms / 1e3) / 1e9
+    tr = ncu_traffic()
     line = {
         "metric": "PIR queries/sec (batched)", "value": qps, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -290,7 +299,9 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": words * 4,
                 "d2h_bytes_per_step": words * 4},
         "roofline": {"kernel": "k_rowsel_tc<64,true> (RowSel, tcgen05 kind::i8)", "bound": "hbm", "achieved": achieved, "peak": hbm,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": tr[0] if tr else None,
+                     "traffic_src": f"profiles/{tr[1]} ({tr[2]}, ncu --set full)" if tr else None,
                      "algorithmic_bytes": rs_bytes, "avg_launch_ms": rs_ms},
         "clocks": clk.summary(),
     }
@@ -364,7 +375,7 @@ def run_rowshard(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))

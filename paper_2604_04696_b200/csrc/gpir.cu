@@ -401,7 +401,11 @@ struct Engine {
       const int mtiles = (M + RA - 1) / RA;
       const bool m64 = RA <= 64;
       const int NT = (m64 && db->d1 >= 64) ? 64 : 32;  // two TMEM accumulator buffers either way
-      const int PST = m64 ? 8 : 4;                     // p per staged epilogue flush
+      static const int pst_env = getenv("GPIR_TC_PST") ? atoi(getenv("GPIR_TC_PST")) : 0;
+      // p per staged epilogue flush: the staging buffer competes with the TMA
+      // pipeline for shared memory, so the M64 x N64 tile stages 4 p (4 stages
+      // in flight) rather than 8 (2 stages)
+      const int PST = (pst_env == 2 || pst_env == 4 || pst_env == 8) ? pst_env : (m64 ? (NT == 64 ? 4 : 8) : 4);
       const int nchunks = ((int)db->d0 + TC_KC - 1) / TC_KC;
       const int ntiles = ((int)db->d1 + NT - 1) / NT;
       if (db->d8_nt != NT) {
@@ -435,7 +439,7 @@ struct Engine {
       const uint32_t stage_bytes = ((4u * RA * TC_KC + 4u * NT * TC_KC) + 127u) & ~127u;
       const size_t outbuf = (size_t)PST * RA * (NT + 1) * 4;
       const size_t fixed = 4096 + outbuf + 2 * TC_MAX_STAGES * 8 + 4 * 8 + 16;
-      ta.stages = std::max(2, std::min<int>(TC_MAX_STAGES, (int)((220u * 1024u - fixed) / stage_bytes)));
+      ta.stages = std::max(2, std::min<int>(TC_MAX_STAGES, (int)((226u * 1024u - fixed) / stage_bytes)));
       const size_t smem = (size_t)ta.stages * stage_bytes + fixed;
       const int grid = std::min(KN / PST, c->num_sms);
       static const bool prof_on = getenv("GPIR_TC_PROF") != nullptr;
@@ -446,8 +450,11 @@ struct Engine {
         CK(cudaMemsetAsync(profbuf.p, 0, profbuf.bytes, s));
         ta.prof = profbuf.as<unsigned long long>();
       }
-      auto kern = NT == 64 ? k_rowsel_tc<64, true, 8>
-                           : (m64 ? k_rowsel_tc<32, true, 8> : k_rowsel_tc<32, false, 4>);
+      auto kern = NT == 64 ? (PST == 8 ? k_rowsel_tc<64, true, 8> : PST == 4 ? k_rowsel_tc<64, true, 4>
+                                                                             : k_rowsel_tc<64, true, 2>)
+                  : m64 ? (PST == 8 ? k_rowsel_tc<32, true, 8> : PST == 4 ? k_rowsel_tc<32, true, 4>
+                                                                          : k_rowsel_tc<32, true, 2>)
+                        : (PST == 2 ? k_rowsel_tc<32, false, 2> : k_rowsel_tc<32, false, 4>);
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<grid, TC_THREADS, smem, s>>>(ta, c->tb);
       CKL();

@@ -77,7 +77,24 @@ __device__ __forceinline__ u32 reduce_u64(u64 x, const Modulus& M) {
   return csub(r, M.q);
 }
 
+// 64-bit MAC accumulator as two independent 32-bit registers.  u64 register
+// pairs must be even-aligned, which inside the NTT loops costs ~100 register
+// moves per transform; the explicit carry chain (IMAD + IMAD.HI.X) does not.
+struct Acc {
+  u32 lo, hi;
+};
+
+__device__ __forceinline__ void acc_zero(Acc& a) { a.lo = a.hi = 0; }
+
+__device__ __forceinline__ void acc_mac(Acc& a, u32 x, u32 y) {
+  asm("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.u32 %1, %2, %3, %1;" : "+r"(a.lo), "+r"(a.hi) : "r"(x), "r"(y));
+}
+
 __device__ __forceinline__ u32 mod_add(u32 a, u32 b, u32 q) { return csub(a + b, q); }
+
+__device__ __forceinline__ u32 reduce_acc(const Acc& a, const Modulus& M) {
+  return reduce_u64(((u64)a.hi << 32) | a.lo, M);
+}
 __device__ __forceinline__ u32 mod_sub(u32 a, u32 b, u32 q) { return csub(a + q - b, q); }
 
 __device__ __forceinline__ u32 mod_mul(u32 a, u32 b, const Modulus& M) {

@@ -45,19 +45,19 @@ __device__ __forceinline__ void st16(u32* p, const u32 (&x)[16]) {
 
 // acc{0,1}[r] += x[r] * row{a,b}[r] over 16 consecutive brv slots, 4 at a time
 __device__ __forceinline__ void mac16(const u32 (&x)[16], const u32* __restrict__ ra, const u32* __restrict__ rb,
-                                      u64 (&acc0)[16], u64 (&acc1)[16]) {
+                                      Acc (&acc0)[16], Acc (&acc1)[16]) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const uint4 a = __ldg(reinterpret_cast<const uint4*>(ra) + c);
     const uint4 b = __ldg(reinterpret_cast<const uint4*>(rb) + c);
-    acc0[4 * c] += (u64)x[4 * c] * a.x;
-    acc0[4 * c + 1] += (u64)x[4 * c + 1] * a.y;
-    acc0[4 * c + 2] += (u64)x[4 * c + 2] * a.z;
-    acc0[4 * c + 3] += (u64)x[4 * c + 3] * a.w;
-    acc1[4 * c] += (u64)x[4 * c] * b.x;
-    acc1[4 * c + 1] += (u64)x[4 * c + 1] * b.y;
-    acc1[4 * c + 2] += (u64)x[4 * c + 2] * b.z;
-    acc1[4 * c + 3] += (u64)x[4 * c + 3] * b.w;
+    acc_mac(acc0[4 * c], x[4 * c], a.x);
+    acc_mac(acc0[4 * c + 1], x[4 * c + 1], a.y);
+    acc_mac(acc0[4 * c + 2], x[4 * c + 2], a.z);
+    acc_mac(acc0[4 * c + 3], x[4 * c + 3], a.w);
+    acc_mac(acc1[4 * c], x[4 * c], b.x);
+    acc_mac(acc1[4 * c + 1], x[4 * c + 1], b.y);
+    acc_mac(acc1[4 * c + 2], x[4 * c + 2], b.z);
+    acc_mac(acc1[4 * c + 3], x[4 * c + 3], b.w);
   }
 }
 
@@ -176,9 +176,9 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
   for (int i = 0; i < K; ++i) {
     const Modulus M = tb.mod[i];
     const u32 q = M.q;
-    u64 acc0[16], acc1[16];
+    Acc acc0[16], acc1[16];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) acc0[r] = acc1[r] = 0;
+    for (int r = 0; r < 16; ++r) acc_zero(acc0[r]), acc_zero(acc1[r]);
 #pragma unroll 1
     for (int j = 0; j < ELL; ++j) {
       const u32* ra = ksk.row(b, j, ELL, CT) + (size_t)i * N;
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
 #ifndef EXP_NO_MAC
             mac16(x, ra + i0, rb + i0, acc0, acc1);
 #else
-            for (int r = 0; r < 16; ++r) acc0[r] += x[r];
+            for (int r = 0; r < 16; ++r) acc0[r].lo += x[r];
 #endif
           });
     }
@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
     u32 xa[16], xb[16], ya[16], yb[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const u32 sa = reduce_u64(acc0[r], M);
-      const u32 sb = mod_add(reduce_u64(acc1[r], M), __ldg(stb + aut_src(i0 + r, k_aut, LOGN)), q);
+      const u32 sa = reduce_acc(acc0[r], M);
+      const u32 sb = mod_add(reduce_acc(acc1[r], M), __ldg(stb + aut_src(i0 + r, k_aut, LOGN)), q);
       xa[r] = mod_add(ca[r], sa, q);
       xb[r] = mod_add(cb[r], sb, q);
       const uint2 w = __ldg(&mono[(size_t)i * N + i0 + r]);
@@ -265,9 +265,9 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
     for (int i = 0; i < K; ++i) {
       const Modulus Mi = tb.mod[i];
       const u32 q = Mi.q;
-      u64 acc0[16], acc1[16];
+      Acc acc0[16], acc1[16];
 #pragma unroll
-      for (int r = 0; r < 16; ++r) acc0[r] = acc1[r] = 0;
+      for (int r = 0; r < 16; ++r) acc_zero(acc0[r]), acc_zero(acc1[r]);
 #pragma unroll 1
       for (int j = 0; j < ELL; ++j) {
         const u32* ra = rows.row(b, comp * ELL + j, ELL, CT) + (size_t)i * N;
@@ -278,15 +278,15 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
   #ifndef EXP_NO_MAC
             mac16(x, ra + i0, rb + i0, acc0, acc1);
 #else
-            for (int r = 0; r < 16; ++r) acc0[r] += x[r];
+            for (int r = 0; r < 16; ++r) acc0[r].lo += x[r];
 #endif
             });
       }
       u32 sa[16], sb[16];
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
-        sa[r] = reduce_u64(acc0[r], Mi);
-        sb[r] = reduce_u64(acc1[r], Mi);
+        sa[r] = reduce_acc(acc0[r], Mi);
+        sb[r] = reduce_acc(acc1[r], Mi);
       }
       u32* da = dst + (size_t)i * N + i0;
       u32* db = dst + (size_t)(K + i) * N + i0;

@@ -17,7 +17,8 @@
 //   D8[p][c][ntile][plane][g][row 32][16 B]  (rows = DB columns, packed once)
 // Work item = (p, NT-column tile, NT = 32 or 64); a persistent CTA per SM runs a multi-stage
 // TMA->MMA pipeline (warp 0 producer, warp 1 single-thread MMA issuer,
-// warps 2-5 epilogue).  With NT = 32 there are two TMEM accumulator buffers
+// warps 2-9 epilogue: two warps per TMEM lane quadrant, each reducing half the
+// columns, with the TMEM loads of the next 8 columns in flight).  With NT = 32 there are two TMEM accumulator buffers
 // (7 x 32 columns each) so the epilogue of one item overlaps the MMAs of the
 // next; NT = 64 halves the A-operand shared-memory reads per MAC instead.
 #pragma once
@@ -27,7 +28,8 @@ namespace gpir {
 
 constexpr int TC_KC = 64;        // K bytes per pipeline stage
 constexpr int TC_MAX_STAGES = 8;
-constexpr int TC_THREADS = 192;  // 6 warps
+constexpr int TC_EPI_WARPS = 8;  // two warps per TMEM lane quadrant, each owning half the columns
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -253,7 +255,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], TC_EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -338,9 +340,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
         }
       }
     }
-  } else {  // epilogue warps 2..5: TMEM lanes 32*(warp%4) .. +31
+  } else {  // epilogue warps 2..9: TMEM lanes 32*(warp%4) .. +31, column half (warp-2)/4
+    constexpr int EPI_T = 32 * TC_EPI_WARPS;
+    constexpr int HC = TC_NT / 2;  // columns per epilogue warp
     const int quad = warp & 3;
-    const int etid = (warp - 2) * 32 + lane;  // 0..127
+    const int half = (warp - 2) >> 2;
+    const int etid = (warp - 2) * 32 + lane;
     int local = 0;
     for (Sched sc; sc.valid(a); sc.next(a), ++local) {
       const int ab = (NBUF == 2) ? (local & 1) : 0;
@@ -349,7 +354,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
       long long e0 = clock64();
       mbar_wait(&tfull[ab], aph);
       long long e1 = clock64();
-      if (a.prof && lane == 0 && quad == 0) a.prof[blockIdx.x * 8 + 3] += e1 - e0;  // epilogue waits
+      if (a.prof && lane == 0 && warp == 2) a.prof[blockIdx.x * 8 + 3] += e1 - e0;  // epilogue waits
       tc_fence_after();
       // tile row held by this thread's TMEM lane for accumulator buffer ab
       const int ml = M64 ? quad * 16 + (lane & 15) : quad * 32 + lane;
@@ -357,33 +362,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
       const bool mine = M64 ? ((lane >> 4) == ab) : true;
       if ((M64 ? quad * 16 : quad * 32) < a.RA) {
         const Modulus M = tb.mod[p >> a.logn];
-        const uint32_t tl = M64 ? tbase + ((uint32_t)(quad * 32) << 16)
-                                : tbase + ((uint32_t)(quad * 32) << 16) + ab * TC_ACC_COLS;
-        u32* orow = outbuf + ((size_t)sc.j * a.RA + ml) * OB_ROW;
-#pragma unroll 1
-        for (int c8 = 0; c8 < TC_NT; c8 += 8) {
-          uint32_t v[7][8];
+        const uint32_t tl = (M64 ? tbase + ((uint32_t)(quad * 32) << 16)
+                                 : tbase + ((uint32_t)(quad * 32) << 16) + ab * TC_ACC_COLS) + half * HC;
+        u32* orow = outbuf + ((size_t)sc.j * a.RA + ml) * OB_ROW + half * HC;
+        const bool act = mine && ml < a.RA && m < a.M;
+        // software pipeline: the TMEM loads of group g+1 are in flight while group g is reduced
+        uint32_t v[2][7][8];
 #pragma unroll
-          for (int u = 0; u < 7; ++u) tmem_ld8(tl + u * TC_NT + c8, v[u]);
-          tmem_ld_wait();
-          if (mine && ml < a.RA && m < a.M) {
+        for (int u = 0; u < 7; ++u) tmem_ld8(tl + u * TC_NT, v[0][u]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < HC / 8; ++g) {
+          const int cb = g & 1;
+          if (g + 1 < HC / 8) {
+#pragma unroll
+            for (int u = 0; u < 7; ++u) tmem_ld8(tl + u * TC_NT + 8 * (g + 1), v[cb ^ 1][u]);
+          }
+          if (act) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               u64 acc = 0;
 #pragma unroll
-              for (int u = 0; u < 7; ++u) acc += (u64)v[u][j] << (8 * u);
-              orow[c8 + j] = reduce_u64(acc, M);
+              for (int u = 0; u < 7; ++u) acc += (u64)v[cb][u][j] << (8 * u);
+              orow[8 * g + j] = reduce_u64(acc, M);
             }
           }
+          if (g + 1 < HC / 8) tmem_ld_wait();
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);  // TMEM buffer free; staging continues
-      if (sc.j == TC_PST - 1) {                 // flush TC_PST consecutive p as 32-byte runs
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (sc.j == TC_PST - 1) {                 // flush TC_PST consecutive p as 16/32-byte runs
+        asm volatile("bar.sync 1, %0;" ::"n"(EPI_T) : "memory");
         const int p0 = sc.blk * TC_PST;
-        for (int w = etid; w < a.RA * TC_NT; w += 128) {
+        for (int w = etid; w < a.RA * TC_NT; w += EPI_T) {
           const int ml = w / TC_NT, cc = w % TC_NT;
           const int mm = sc.mt * a.RA + ml;
           const int n = nt * TC_NT + cc;
@@ -391,14 +404,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
             u32 o[TC_PST];
 #pragma unroll
             for (int j = 0; j < TC_PST; ++j) o[j] = outbuf[((size_t)j * a.RA + ml) * OB_ROW + cc];
-            uint4* dst = reinterpret_cast<uint4*>(a.out + (((size_t)(mm >> 1) * a.d1 + n) * 2 + (mm & 1)) * a.KN + p0);
+            u32* dw = a.out + (((size_t)(mm >> 1) * a.d1 + n) * 2 + (mm & 1)) * a.KN + p0;
+            if constexpr (TC_PST >= 4) {
+              uint4* dst = reinterpret_cast<uint4*>(dw);
 #pragma unroll
-            for (int v = 0; v < TC_PST / 4; ++v) dst[v] = make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+              for (int v = 0; v < TC_PST / 4; ++v) dst[v] = make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+            } else {
+              *reinterpret_cast<uint2*>(dw) = make_uint2(o[0], o[1]);
+            }
           }
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(EPI_T) : "memory");
       }
-      if (a.prof && lane == 0 && quad == 0) a.prof[blockIdx.x * 8 + 4] += clock64() - e1;  // epilogue work
+      if (a.prof && lane == 0 && warp == 2) a.prof[blockIdx.x * 8 + 4] += clock64() - e1;  // epilogue work
     }
   }
   __syncthreads();

@@ -128,8 +128,8 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
 // prefetched into smem while digit j is transformed.
 template <int LOGN, int K, class RowFn>
 __device__ __forceinline__ void k2_mac(NttState& ns, u32* keys, uint64_t* kbar, const int* __restrict__ dig, int ndig,
-                                       int i, RowFn&& row, const Tables& tb, const TwConst& tc, u64 (&acc0)[16],
-                                       u64 (&acc1)[16]) {
+                                       int i, RowFn&& row, const Tables& tb, const TwConst& tc, Acc (&acc0)[16],
+                                       Acc (&acc1)[16]) {
   constexpr int N = 1 << LOGN, SH = NttCfg<LOGN>::SHIFT;
   const int tid = threadIdx.x;
   const Modulus& Mi = tb.mod[i];
@@ -145,7 +145,7 @@ __device__ __forceinline__ void k2_mac(NttState& ns, u32* keys, uint64_t* kbar, 
   };
   if (tid == 0) prefetch(0);
 #pragma unroll
-  for (int r = 0; r < 16; ++r) acc0[r] = acc1[r] = 0;
+  for (int r = 0; r < 16; ++r) acc_zero(acc0[r]), acc_zero(acc1[r]);
 #pragma unroll 1
   for (int j = 0; j < ndig; ++j) {
     __syncthreads();  // every thread is past the MAC of digit j-1: its key buffer may be refilled
@@ -161,14 +161,14 @@ __device__ __forceinline__ void k2_mac(NttState& ns, u32* keys, uint64_t* kbar, 
           for (int c = 0; c < 4; ++c) {
             const uint4 a = *reinterpret_cast<const uint4*>(ka + 4 * c);
             const uint4 b = *reinterpret_cast<const uint4*>(kb + 4 * c);
-            acc0[4 * c] += (u64)x[4 * c] * a.x;
-            acc0[4 * c + 1] += (u64)x[4 * c + 1] * a.y;
-            acc0[4 * c + 2] += (u64)x[4 * c + 2] * a.z;
-            acc0[4 * c + 3] += (u64)x[4 * c + 3] * a.w;
-            acc1[4 * c] += (u64)x[4 * c] * b.x;
-            acc1[4 * c + 1] += (u64)x[4 * c + 1] * b.y;
-            acc1[4 * c + 2] += (u64)x[4 * c + 2] * b.z;
-            acc1[4 * c + 3] += (u64)x[4 * c + 3] * b.w;
+            acc_mac(acc0[4 * c], x[4 * c], a.x);
+            acc_mac(acc0[4 * c + 1], x[4 * c + 1], a.y);
+            acc_mac(acc0[4 * c + 2], x[4 * c + 2], a.z);
+            acc_mac(acc0[4 * c + 3], x[4 * c + 3], a.w);
+            acc_mac(acc1[4 * c], x[4 * c], b.x);
+            acc_mac(acc1[4 * c + 1], x[4 * c + 1], b.y);
+            acc_mac(acc1[4 * c + 2], x[4 * c + 2], b.z);
+            acc_mac(acc1[4 * c + 3], x[4 * c + 3], b.w);
           }
         });
   }
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, 2)
   const int gn = node0 + ln;
   const int b = gn / C, c = gn % C;
   const size_t CT = 2 * (size_t)K * N;
-  u64 acc0[16], acc1[16];
+  Acc acc0[16], acc1[16];
   k2_mac<LOGN, K>(ns, keys, kbar, dig + (size_t)ln * ELL * N, ELL, i,
                   [&](int j) { return ksk.row(b, j, ELL, CT); }, tb, tc, acc0, acc1);
   // combine (src/planner.py:361-363): out[c] = state + s, out[c + C] = X^-2^t (state - s)
@@ -222,8 +222,8 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, 2)
   u32 xa[16], xb[16], ya[16], yb[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
-    const u32 sa = reduce_u64(acc0[r], M);
-    const u32 sb = mod_add(reduce_u64(acc1[r], M), __ldg(stb + aut_src(i0 + r, k_aut, LOGN)), q);
+    const u32 sa = reduce_acc(acc0[r], M);
+    const u32 sb = mod_add(reduce_acc(acc1[r], M), __ldg(stb + aut_src(i0 + r, k_aut, LOGN)), q);
     xa[r] = mod_add(ca[r], sa, q);
     xb[r] = mod_add(cb[r], sb, q);
     const uint2 w = __ldg(&mono[(size_t)i * N + i0 + r]);
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, 2)
   const int g = m0 + lc;
   const int b = g / M_per_b, m = g % M_per_b;
   const size_t CT = 2 * (size_t)K * N;
-  u64 acc0[16], acc1[16];
+  Acc acc0[16], acc1[16];
   // digits: a-component's ELL then b-component's ELL, matching rows [0, 2 ELL)
   k2_mac<LOGN, K>(ns, keys, kbar, dig + (size_t)lc * 2 * ELL * N, 2 * ELL, i,
                   [&](int j) { return rows.row(b, j, ELL, CT); }, tb, tc, acc0, acc1);
@@ -266,8 +266,8 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, 2)
   u32 sa[16], sb[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
-    sa[r] = reduce_u64(acc0[r], M);
-    sb[r] = reduce_u64(acc1[r], M);
+    sa[r] = reduce_acc(acc0[r], M);
+    sb[r] = reduce_acc(acc1[r], M);
   }
   if (pairs) {  // coltor_stage: even + (odd - even) ⊡ rgsw (src/planner.py:457-463)
     const u32* ev = in + (b * in_b + 2 * (size_t)m) * CT;
