@@ -173,6 +173,8 @@ static int build_tables(gpir_ctx* c) {
     for (int it = 0; it < 5; ++it) inv32 *= 2 - q * inv32;
     M.qinv_neg = (uint32_t)(0u - inv32);
     M.r2 = (uint32_t)((((u128)1) << 64) % q);
+    M.r1 = (uint32_t)((1ull << 32) % q);
+    M.r1_sh = shoup(M.r1, q);
     M.barrett = (uint32_t)((1ull << 32) / q);
     M.ninv = (uint32_t)powmod(n, q - 2, q);
     M.ninv_sh = shoup(M.ninv, q);
@@ -208,6 +210,10 @@ static int build_tables(gpir_ctx* c) {
     ++cc.n_red;
     t /= 2;
   }
+  u128 dc = 0;
+  for (uint32_t j = 0; j + 1 < c->ell; ++j) dc += (((u128)1 << (c->z_bits - 1)) - 1) << (c->z_bits * j);
+  cc.dc_lo = (uint64_t)dc;
+  cc.dc_hi = (uint64_t)(dc >> 64);
   int rc;
   if ((rc = c->tw_fwd.ensure(fwd.size() * sizeof(uint2)))) return rc;
   if ((rc = c->tw_inv.ensure(inv.size() * sizeof(uint2)))) return rc;
@@ -248,7 +254,7 @@ struct Engine {
   static constexpr int T = NttCfg<LOGN>::T;
   static constexpr size_t CT = 2 * (size_t)K * N;
   static size_t fused_smem() {
-    return (size_t)NttCfg<LOGN>::XBUF_WORDS * 4 + (size_t)priv_slots<K, ELL>() * 16 * T * 4;
+    return (size_t)NttCfg<LOGN>::XBUF_WORDS * 4 + (size_t)priv_slots<K, ELL>() * 16 * T * 4 + 16;  // + mbarrier
   }
 
   static int setup_attrs() {

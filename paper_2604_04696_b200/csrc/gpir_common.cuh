@@ -30,6 +30,8 @@ struct Modulus {
   u32 ninv_sh;    // Shoup companion of ninv
   u32 mhat;       // (Q/q)^{-1} mod q   (CRT, src/ring.py:216-220)
   u32 mhat_sh;
+  u32 r1;         // 2^32 mod q (undoes the Montgomery factor of mont_mac)
+  u32 r1_sh;
 };
 
 // CRT / gadget constants (src/ring.py:214-235, src/he.py:45-55).
@@ -43,6 +45,7 @@ struct CrtConst {
   u64 half_lo, half_hi;                   // (Q-1)/2
   int n_red;                              // descending multiples t*Q to subtract
   u64 red_lo[4], red_hi[4];
+  u64 dc_lo, dc_hi;                       // sum_{j < ell-1} (z/2 - 1) z^j (closed-form digits)
 };
 
 // Device-resident transform tables for one context.
@@ -87,10 +90,29 @@ struct Acc {
 __device__ __forceinline__ void acc_zero(Acc& a) { a.lo = a.hi = 0; }
 
 __device__ __forceinline__ void acc_mac(Acc& a, u32 x, u32 y) {
-  asm("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.u32 %1, %2, %3, %1;" : "+r"(a.lo), "+r"(a.hi) : "r"(x), "r"(y));
+  asm("{\n\t.reg .u32 h;\n\tmul.hi.u32 h, %2, %3;\n\tmad.lo.cc.u32 %0, %2, %3, %0;\n\taddc.u32 %1, %1, h;\n\t}"
+      : "+r"(a.lo), "+r"(a.hi)
+      : "r"(x), "r"(y));
 }
 
 __device__ __forceinline__ u32 mod_add(u32 a, u32 b, u32 q) { return csub(a + b, q); }
+
+// Signed lazy Montgomery MAC: acc += x*y*2^-32 mod q, exactly representable:
+// with m = lo(x*y) * q^-1 mod 2^32 the low words of x*y and m*q agree, so
+// (x*y - m*q) / 2^32 = hi(x*y) - hi(m*q), which lies in (-q, q) for any
+// 32-bit x and y < q.  Four IMAD-class ops and a 32-bit accumulator (no
+// 64-bit register pairs); `terms` such products stay in int32 while
+// terms * q < 2^31.
+__device__ __forceinline__ void mont_mac(int& acc, u32 x, u32 y, u32 q, u32 qinv) {
+  const u32 lo = x * y, hi = __umulhi(x, y);
+  acc += (int)(hi - __umulhi(lo * qinv, q));
+}
+
+// canonical (acc * 2^32) mod q for an accumulator of `terms` mont_mac terms
+__device__ __forceinline__ u32 mont_fin(int acc, int terms, const Modulus& M) {
+  const u32 v = (u32)(acc + terms * (int)M.q);  // in (0, 2 terms q)
+  return csub(mul_shoup(v, M.r1, M.r1_sh, M.q), M.q);
+}
 
 __device__ __forceinline__ u32 reduce_acc(const Acc& a, const Modulus& M) {
   return reduce_u64(((u64)a.hi << 32) | a.lo, M);

@@ -5,6 +5,7 @@
 // (gpir_common.cuh).  Template parameters: LOGN = log2 n, K = RNS limbs,
 // ELL = gadget digits.
 #pragma once
+#include "async.cuh"
 #include "ntt.cuh"
 
 namespace gpir {
@@ -61,12 +62,138 @@ __device__ __forceinline__ void mac16(const u32 (&x)[16], const u32* __restrict_
   }
 }
 
+// 16 consecutive key words of one row, fetched before the transform that
+// consumes them so the L2 latency hides behind the butterflies
+struct Key16 {
+  uint4 v[4];
+  __device__ __forceinline__ void load(const u32* __restrict__ p) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = __ldg(reinterpret_cast<const uint4*>(p) + c);
+  }
+  __device__ __forceinline__ u32 operator[](int r) const {
+    const uint4& t = v[r >> 2];
+    return (r & 3) == 0 ? t.x : (r & 3) == 1 ? t.y : (r & 3) == 2 ? t.z : t.w;
+  }
+};
+
+// acc{0,1}[r] += x[r] * k{a,b}[r] * 2^-32 (mont_mac) for lazy NTT outputs x
+__device__ __forceinline__ void mont_mac16(const u32 (&x)[16], const Key16& ka, const Key16& kb, int (&acc0)[16],
+                                           int (&acc1)[16], u32 q, u32 qinv) {
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    mont_mac(acc0[r], x[r], ka[r], q, qinv);
+    mont_mac(acc1[r], x[r], kb[r], q, qinv);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // CRT + centered digits for one coefficient (src/ring.py:456-495,
 // src/he.py:346-362): exact 128-bit reconstruction into [0, Q), centering to
 // sign/magnitude, then base-2^z_bits digits with the sign-magnitude carry rule.
+//
+// Fast path (z = 22, 4-word arithmetic on PTX carry chains): S = sum y_i Q/q_i
+// < K Q, reduced by the descending multiples of Q; centered; then the
+// carry-rule digits in closed form: with T = mag + sum_{j<ell-1} (z/2-1) z^j,
+// digit j < ell-1 is bits [jz, jz+z) of T minus (z/2 - 1) and the last digit
+// is T >> (ell-1) z (the rule keeps raw == z/2 positive, so the balanced
+// digits lie in [-z/2+1, z/2]; checked exhaustively on the boundary patterns
+// against the reference loop in tests/test_oracle.py).
+struct W4 {
+  u32 w0, w1, w2, w3;
+};
+
+__device__ __forceinline__ W4 w4(u64 lo, u64 hi) { return W4{(u32)lo, (u32)(lo >> 32), (u32)hi, (u32)(hi >> 32)}; }
+
+// S += y * M  (mod 2^128)
+__device__ __forceinline__ void w4_mac(W4& S, u32 y, const W4& M) {
+  asm("mad.lo.cc.u32 %0, %4, %5, %0;\n\t"
+      "madc.lo.cc.u32 %1, %4, %6, %1;\n\t"
+      "madc.lo.cc.u32 %2, %4, %7, %2;\n\t"
+      "madc.lo.u32 %3, %4, %8, %3;\n\t"
+      "mad.hi.cc.u32 %1, %4, %5, %1;\n\t"
+      "madc.hi.cc.u32 %2, %4, %6, %2;\n\t"
+      "madc.hi.u32 %3, %4, %7, %3;"
+      : "+r"(S.w0), "+r"(S.w1), "+r"(S.w2), "+r"(S.w3)
+      : "r"(y), "r"(M.w0), "r"(M.w1), "r"(M.w2), "r"(M.w3));
+}
+
+// D = A - B; returns the borrow (A < B)
+__device__ __forceinline__ bool w4_sub(W4& D, const W4& A, const W4& B) {
+  u32 br;
+  asm("sub.cc.u32 %0, %5, %9;\n\t"
+      "subc.cc.u32 %1, %6, %10;\n\t"
+      "subc.cc.u32 %2, %7, %11;\n\t"
+      "subc.cc.u32 %3, %8, %12;\n\t"
+      "subc.u32 %4, 0, 0;"
+      : "=r"(D.w0), "=r"(D.w1), "=r"(D.w2), "=r"(D.w3), "=r"(br)
+      : "r"(A.w0), "r"(A.w1), "r"(A.w2), "r"(A.w3), "r"(B.w0), "r"(B.w1), "r"(B.w2), "r"(B.w3));
+  return br != 0;
+}
+
+__device__ __forceinline__ W4 w4_add(const W4& A, const W4& B) {
+  W4 D;
+  asm("add.cc.u32 %0, %4, %8;\n\t"
+      "addc.cc.u32 %1, %5, %9;\n\t"
+      "addc.cc.u32 %2, %6, %10;\n\t"
+      "addc.u32 %3, %7, %11;"
+      : "=r"(D.w0), "=r"(D.w1), "=r"(D.w2), "=r"(D.w3)
+      : "r"(A.w0), "r"(A.w1), "r"(A.w2), "r"(A.w3), "r"(B.w0), "r"(B.w1), "r"(B.w2), "r"(B.w3));
+  return D;
+}
+
+__device__ __forceinline__ W4 w4_sel(bool p, const W4& A, const W4& B) {
+  return W4{p ? A.w0 : B.w0, p ? A.w1 : B.w1, p ? A.w2 : B.w2, p ? A.w3 : B.w3};
+}
+
+// bits [s, s + 32) of T, s a compile-time constant
+template <int S>
+__device__ __forceinline__ u32 w4_bits(const W4& T) {
+  constexpr int w = S >> 5, o = S & 31;
+  const u32 lo = w == 0 ? T.w0 : w == 1 ? T.w1 : w == 2 ? T.w2 : T.w3;
+  const u32 hi = w == 0 ? T.w1 : w == 1 ? T.w2 : w == 2 ? T.w3 : 0u;
+  return o == 0 ? lo : __funnelshift_r(lo, hi, o);
+}
+
+template <int ZB, int ELL, int J = 0>
+__device__ __forceinline__ void w4_digits(const W4& T, u32 sgn, int (&d)[ELL]) {
+  if constexpr (J < ELL) {
+    int v;
+    if constexpr (J < ELL - 1)
+      v = (int)(w4_bits<J * ZB>(T) & ((1u << ZB) - 1)) - ((1 << (ZB - 1)) - 1);
+    else
+      v = (int)w4_bits<J * ZB>(T);
+    d[J] = (v ^ (int)sgn) - (int)sgn;  // sgn = 0 or -1
+    w4_digits<ZB, ELL, J + 1>(T, sgn, d);
+  }
+}
+
 template <int K, int ELL>
 __device__ __forceinline__ void dcp_coeff(const u32 (&c)[K], int (&d)[ELL], const Tables& tb, const CrtConst& cc) {
+  if (cc.z_bits == 22 && ELL * 22 <= 128) {
+    W4 S{0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const Modulus& M = tb.mod[i];
+      const u32 y = csub(mul_shoup(c[i], M.mhat, M.mhat_sh, M.q), M.q);
+      w4_mac(S, y, w4(cc.m_lo[i], cc.m_hi[i]));
+    }
+    // S < K Q <= P Q (P = next power of two >= K): subtract P/2 Q, ..., 2 Q, Q
+    // conditionally (cc.red holds P Q, P/2 Q, ..., Q; the first is never needed)
+    constexpr int NR = K <= 1 ? 0 : K <= 2 ? 1 : K <= 4 ? 2 : 3;
+#pragma unroll
+    for (int t = 1; t <= NR; ++t) {
+      W4 D;
+      const bool br = w4_sub(D, S, w4(cc.red_lo[t], cc.red_hi[t]));
+      S = w4_sel(br, S, D);
+    }
+    W4 D, mag;
+    const bool pos = !w4_sub(D, w4(cc.half_lo, cc.half_hi), S);  // S <= (Q-1)/2
+    w4_sub(D, w4(cc.q_lo, cc.q_hi), S);
+    mag = w4_sel(pos, S, D);
+    const W4 T = w4_add(mag, w4(cc.dc_lo, cc.dc_hi));
+    w4_digits<22, ELL>(T, pos ? 0u : ~0u, d);
+    return;
+  }
   typedef unsigned __int128 u128;
   u128 X = 0;
 #pragma unroll
@@ -143,24 +270,35 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
   extern __shared__ __align__(16) u32 smem[];
   NttState ns{smem, 0};
   int* priv = reinterpret_cast<int*>(smem + NttCfg<LOGN>::XBUF_WORDS);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(priv + priv_slots<K, ELL>() * 16 * T);
   const int tid = threadIdx.x;
   const int node = blockIdx.x;
   const int b = node / C, c = node % C;
   const size_t CT = 2 * (size_t)K * N;
   const u32* st = state + ((size_t)b * C + c) * CT;
 
+  // all K limbs of `a` land in private slots 0..K-1 with one bulk copy each;
+  // the iNTT of limb i gathers (automorphism) from slot i and writes its
+  // coefficients back into slot i (a block barrier separates the two)
+  static_assert(priv_slots<K, ELL>() >= K, "slot per limb");
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(bar, (uint32_t)(K * N * 4));
+#pragma unroll 1
+    for (int i = 0; i < K; ++i) bulk_g2s(priv + i * 16 * T, st + (size_t)i * N, N * 4, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+
 #pragma unroll 1
   for (int i = 0; i < K; ++i) {
-    __syncthreads();
-    const uint4* src = reinterpret_cast<const uint4*>(st + (size_t)i * N);
-    u32* stage_buf = stage_buffer<LOGN>(ns);  // not touched by the next transform
-    for (int v = tid; v < N / 4; v += T) reinterpret_cast<uint4*>(stage_buf)[v] = __ldg(src + v);
-    __syncthreads();
+    const u32* slot = reinterpret_cast<const u32*>(priv + i * 16 * T);
     ntt_inv<LOGN>(
         ns, tb.inv + (size_t)i * N, tc.i[i], tb.mod[i],
         [&](int i0, u32(&x)[16]) {
 #pragma unroll
-          for (int r = 0; r < 16; ++r) x[r] = stage_buf[aut_src(i0 + r, k_aut, LOGN)];
+          for (int r = 0; r < 16; ++r) x[r] = slot[aut_src(i0 + r, k_aut, LOGN)];
         },
         [&](int, int r, u32 v) { priv[pv<T>(i, r)] = (int)v; });
   }
@@ -176,32 +314,34 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
   for (int i = 0; i < K; ++i) {
     const Modulus M = tb.mod[i];
     const u32 q = M.q;
-    Acc acc0[16], acc1[16];
+    const u32 qinv = 0u - M.qinv_neg;
+    const u32* stb = st + (size_t)(K + i) * N;
+    u32 gb[16];
+    int acc0[16], acc1[16];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) acc_zero(acc0[r]), acc_zero(acc1[r]);
+    for (int r = 0; r < 16; ++r) acc0[r] = acc1[r] = 0;
 #pragma unroll 1
     for (int j = 0; j < ELL; ++j) {
       const u32* ra = ksk.row(b, j, ELL, CT) + (size_t)i * N;
-      const u32* rb = ra + (size_t)K * N;
-      ntt_fwd<LOGN>(
+      Key16 ka, kb;
+      ka.load(ra + i0);
+      kb.load(ra + (size_t)K * N + i0);
+      if (j == ELL - 1) {  // the automorphism gather of b for the combine, in flight during the last transform
+#pragma unroll
+        for (int r = 0; r < 16; ++r) gb[r] = __ldg(stb + aut_src(i0 + r, k_aut, LOGN));
+      }
+      ntt_fwd<LOGN, true>(
           ns, tb.fwd + (size_t)i * N, tc.f[i], M, [&](int jj) -> u32 { return lift(priv[pv<T>(j, jj >> SH)], q); },
-          [&](int, const u32(&x)[16]) {
-#ifndef EXP_NO_MAC
-            mac16(x, ra + i0, rb + i0, acc0, acc1);
-#else
-            for (int r = 0; r < 16; ++r) acc0[r].lo += x[r];
-#endif
-          });
+          [&](int, const u32(&x)[16]) { mont_mac16(x, ka, kb, acc0, acc1, q, qinv); });
     }
     u32 ca[16], cb[16];
     ld16(st + (size_t)i * N + i0, ca);
     ld16(st + (size_t)(K + i) * N + i0, cb);
-    const u32* stb = st + (size_t)(K + i) * N;
     u32 xa[16], xb[16], ya[16], yb[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const u32 sa = reduce_acc(acc0[r], M);
-      const u32 sb = mod_add(reduce_acc(acc1[r], M), __ldg(stb + aut_src(i0 + r, k_aut, LOGN)), q);
+      const u32 sa = mont_fin(acc0[r], ELL, M);
+      const u32 sb = mod_add(mont_fin(acc1[r], ELL, M), gb[r], q);
       xa[r] = mod_add(ca[r], sa, q);
       xb[r] = mod_add(cb[r], sb, q);
       const uint2 w = __ldg(&mono[(size_t)i * N + i0 + r]);
@@ -265,28 +405,25 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
     for (int i = 0; i < K; ++i) {
       const Modulus Mi = tb.mod[i];
       const u32 q = Mi.q;
-      Acc acc0[16], acc1[16];
+      const u32 qinv = 0u - Mi.qinv_neg;
+      int acc0[16], acc1[16];
 #pragma unroll
-      for (int r = 0; r < 16; ++r) acc_zero(acc0[r]), acc_zero(acc1[r]);
+      for (int r = 0; r < 16; ++r) acc0[r] = acc1[r] = 0;
 #pragma unroll 1
       for (int j = 0; j < ELL; ++j) {
         const u32* ra = rows.row(b, comp * ELL + j, ELL, CT) + (size_t)i * N;
-        const u32* rb = ra + (size_t)K * N;
-        ntt_fwd<LOGN>(
+        Key16 ka, kb;
+        ka.load(ra + i0);
+        kb.load(ra + (size_t)K * N + i0);
+        ntt_fwd<LOGN, true>(
             ns, tb.fwd + (size_t)i * N, tc.f[i], Mi, [&](int jj) -> u32 { return lift(priv[pv<T>(j, jj >> SH)], q); },
-            [&](int, const u32(&x)[16]) {
-  #ifndef EXP_NO_MAC
-            mac16(x, ra + i0, rb + i0, acc0, acc1);
-#else
-            for (int r = 0; r < 16; ++r) acc0[r].lo += x[r];
-#endif
-            });
+            [&](int, const u32(&x)[16]) { mont_mac16(x, ka, kb, acc0, acc1, q, qinv); });
       }
       u32 sa[16], sb[16];
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
-        sa[r] = reduce_acc(acc0[r], Mi);
-        sb[r] = reduce_acc(acc1[r], Mi);
+        sa[r] = mont_fin(acc0[r], ELL, Mi);
+        sb[r] = mont_fin(acc1[r], ELL, Mi);
       }
       u32* da = dst + (size_t)i * N + i0;
       u32* db = dst + (size_t)(K + i) * N + i0;

@@ -232,7 +232,9 @@ __device__ __forceinline__ void fwd_passes(u32* buf, u32 (&x)[16], int tid, cons
   }
 }
 
-template <int LOGN, class LD, class ST>
+// LAZY: hand st() the unreduced outputs (< (2 LOGN + 1) q < 2^32 for 27-bit q),
+// for consumers that accept any 32-bit operand (mont_mac).
+template <int LOGN, bool LAZY = false, class LD, class ST>
 __device__ __forceinline__ void ntt_fwd(NttState& ns, const uint2* __restrict__ twg, const uint2* twc,
                                         const Modulus& M, LD&& ld, ST&& st) {
   using C = NttCfg<LOGN>;
@@ -247,10 +249,12 @@ __device__ __forceinline__ void ntt_fwd(NttState& ns, const uint2* __restrict__ 
 #ifndef EXP_NO_FWD
     fwd_passes<LOGN, LOGN - 4>(buf, x, tid, twg, twc, q);
 #endif
+    if constexpr (!LAZY) {
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {  // x < (2 LOGN + 1) q: Barrett to [0, 2q), then canonical
-      const u32 v = x[r] - mulhi(x[r], M.barrett) * q;
-      x[r] = csub(v, q);
+      for (int r = 0; r < 16; ++r) {  // x < (2 LOGN + 1) q: Barrett to [0, 2q), then canonical
+        const u32 v = x[r] - mulhi(x[r], M.barrett) * q;
+        x[r] = csub(v, q);
+      }
     }
     st(tid << 4, x);
   } else {
