@@ -62,7 +62,9 @@ __device__ __forceinline__ u32 mul_shoup(u32 x, u32 w, u32 wsh, u32 q) {
   return x * w - mulhi(x, wsh) * q;
 }
 
-__device__ __forceinline__ u32 csub(u32 x, u32 m) { return x >= m ? x - m : x; }
+// x < 2m <= 2^32 -> x mod m as an unsigned min (one ALU VIMNMX instead of
+// ISETP + SEL): if x < m, x - m wraps above x.
+__device__ __forceinline__ u32 csub(u32 x, u32 m) { return min(x, x - m); }
 
 // Montgomery REDC: u < q * 2^32  ->  u * 2^-32 mod q in [0, 2q).
 __device__ __forceinline__ u32 redc(u64 u, const Modulus& M) {

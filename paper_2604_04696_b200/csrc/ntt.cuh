@@ -159,13 +159,16 @@ __device__ __forceinline__ void fwd_stage(u32 (&x)[16], int tid, const uint2* __
   const int off = (1 << S) + (tpart<LOGN, B0>(tid) << (3 - RB));
   load_tw<B0, RB>((B0 == 0 ? twg : twc) + off, w);
   const u32 q2 = 2 * q;
+  const u32 zero = q >> 31;  // 0 (q < 2^31), opaque to the compiler
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
     if (r & (1 << RB)) continue;
     const uint2 ww = w[r >> (RB + 1)];
     const u32 u = x[r];
     const u32 t = mul_shoup(x[r | (1 << RB)], ww.x, ww.y, q);
-    x[r] = u + t;
+    // u + t as max(u + t, 0): keeps the add on the ALU pipe (VIADDMNMX)
+    // instead of an IMAD.IADD competing with the multiplies for the FMA pipe
+    x[r] = __viaddmax_u32(u, t, zero);
     x[r | (1 << RB)] = u + q2 - t;
   }
 }
