@@ -206,9 +206,16 @@ def run_ours(args, rank, world, local_rank):
     em = np.zeros(16, np.uint8)
     cm = np.zeros(16, np.uint8)
     nat.check(lib.gpir_plan(ctx.h, d0, d1, B, nat.ptr(em, C.c_uint8), 16, nat.ptr(cm, C.c_uint8), 16), "plan")
-    if args.modes:
+    if args.modes in ("fused", "op"):
         em[:] = 1 if args.modes == "fused" else 0
         cm[:] = em[0]
+    elif args.modes:  # explicit per-stage plan "EQ/CT", chars o (op-level), F (fused), S (split), H (op iNTT+Dcp, fused NTT+MAC)
+        code = {"o": 0, "F": 1, "S": 2, "H": 3}
+        eq, ct = args.modes.split("/")
+        for i, ch in enumerate(eq):
+            em[i] = code[ch]
+        for i, ch in enumerate(ct):
+            cm[i] = code[ch]
     st = nat.GpirStats()
 
     def step(stats=None):
@@ -379,7 +386,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
-    ap.add_argument("--modes", default="", choices=["", "fused", "op"])
+    ap.add_argument("--modes", default="", help='"fused", "op", or an explicit plan "EQ/CT" (o/F/S/H per stage)')
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--strategy", default="replica", choices=["replica", "rowshard"],
                     help="multi-GPU mode: replica (DB copy + own batch per GPU) or rowshard (north-star DB row shards)")

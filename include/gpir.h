@@ -25,7 +25,10 @@
  * mutex per context).  Stage modes: 0 = operation-level, 1 = stage-fused
  * (planner.ExecMode OPERATION_LEVEL / STAGE_LEVEL, src/planner.py:105-107),
  * 2 = split stage-fused (per-node iNTT+Dcp kernel, per node x limb NTT+MAC
- * kernel; experimental, bit-identical).
+ * kernel), 3 = hybrid (operation-level iNTT and Dcp, then the per node x limb
+ * NTT+MAC kernel); all bit-identical.  Key rows are stored with the top gadget
+ * digit folded in (see k_fold_rows), so ell-1 digits per component are
+ * transformed.
  */
 #ifndef GPIR_H
 #define GPIR_H

@@ -18,6 +18,10 @@
 #include "rowsel_tc.cuh"
 #include "stage_kernels.cuh"
 
+// hybrid planner thresholds (nodes / ciphertexts per stage, whole batch)
+static constexpr size_t kEqStageNodes = 2048;
+static constexpr size_t kXpStageCts = 256;
+
 using namespace gpir;
 
 static thread_local std::string g_err;
@@ -94,6 +98,7 @@ struct gpir_ctx {
   Tables tb{};
   CrtConst cc{};
   TwConst tc{};
+  FoldConst fc{};
   DevBuf tw_fwd, tw_inv, mono;
   // key pool
   uint32_t key_slots = 0, key_stages = 0;
@@ -101,7 +106,7 @@ struct gpir_ctx {
   std::vector<char> slot_rgsw;
   DevBuf evk_pool, rgsw_pool;
   // workspace
-  DevBuf ws_state0, ws_state1, ws_arows, ws_sel, ws_ct0, ws_ct1, ws_kslot;
+  DevBuf ws_state0, ws_state1, ws_arows, ws_sel, ws_ct0, ws_ct1, ws_kslot, ws_crows;
   DevBuf ws_coeff, ws_dig, ws_dn, ws_io0, ws_io1, ws_a8;
   int rowsel_engine = 0;  // 0 auto, 1 CUDA cores, 2 tensor cores
   int num_sms = 148;
@@ -214,6 +219,16 @@ static int build_tables(gpir_ctx* c) {
   for (uint32_t j = 0; j + 1 < c->ell; ++j) dc += (((u128)1 << (c->z_bits - 1)) - 1) << (c->z_bits * j);
   cc.dc_lo = (uint64_t)dc;
   cc.dc_hi = (uint64_t)(dc >> 64);
+  // top-digit fold constants (k_fold_rows): z^(j-(ell-1)) and z^-(ell-1) mod q_i
+  for (uint32_t i = 0; i < k; ++i) {
+    const uint64_t qi = c->q[i];
+    const uint64_t zinv = powmod(powmod(2, c->z_bits, qi), qi - 2, qi);
+    for (uint32_t j = 0; j < c->ell; ++j) {
+      const uint32_t e = (j + 1 < c->ell) ? c->ell - 1 - j : c->ell - 1;
+      const uint32_t w = (uint32_t)powmod(zinv, e, qi);
+      c->fc.w[i][j] = make_uint2(w, shoup(w, (uint32_t)qi));
+    }
+  }
   int rc;
   if ((rc = c->tw_fwd.ensure(fwd.size() * sizeof(uint2)))) return rc;
   if ((rc = c->tw_inv.ensure(inv.size() * sizeof(uint2)))) return rc;
@@ -248,6 +263,58 @@ static int bitrev_rows(gpir_ctx* c, const uint32_t* in, uint32_t* out, size_t ro
   return 0;
 }
 
+// Top-digit fold (k_fold_rows) of B x G row groups of ell rows each: group
+// (b, g) at src + b*sb + g*sg -> dst + b*db + g*dg (words; may alias).
+static int fold_rows(gpir_ctx* c, const uint32_t* src, uint32_t* dst, int B, int G, size_t sb, size_t sg, size_t db,
+                     size_t dg, cudaStream_t s) {
+  const size_t tot = (size_t)B * G * (2 * (size_t)c->k << c->logn);
+  if (!tot) return 0;
+  const unsigned grid = (unsigned)((tot + 255) / 256);
+  switch (c->ell) {
+    case 5:
+      k_fold_rows<5><<<grid, 256, 0, s>>>(src, dst, B, G, sb, sg, db, dg, (int)c->logn, (int)c->k, c->tb, c->fc);
+      break;
+    case 6:
+      k_fold_rows<6><<<grid, 256, 0, s>>>(src, dst, B, G, sb, sg, db, dg, (int)c->logn, (int)c->k, c->tb, c->fc);
+      break;
+    default:
+      FAIL(GPIR_UNSUPPORTED, "fold: unsupported ell");
+  }
+  CKL();
+  return 0;
+}
+
+// Per-stage device timing for plan tuning (GPIR_STAGE_PROF=1): events on the
+// launch stream, printed to stderr at the end of each batch.
+struct StageProf {
+  bool on = getenv("GPIR_STAGE_PROF") != nullptr;
+  std::vector<cudaEvent_t> ev;
+  std::vector<std::string> lab;
+  size_t n = 0;
+  void mark(cudaStream_t s, const std::string& l) {
+    if (!on) return;
+    if (n == ev.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+      lab.emplace_back();
+    }
+    lab[n] = l;
+    cudaEventRecord(ev[n++], s);
+  }
+  void flush() {
+    if (!on || n < 2) return;
+    cudaEventSynchronize(ev[n - 1]);
+    for (size_t i = 1; i < n; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      fprintf(stderr, "[stage prof] %-16s %8.3f ms\n", lab[i].c_str(), ms);
+    }
+    n = 0;
+  }
+};
+static thread_local StageProf g_sprof;
+
 template <int LOGN, int K, int ELL>
 struct Engine {
   static constexpr int N = 1 << LOGN;
@@ -263,10 +330,6 @@ struct Engine {
     const int sm = (int)fused_smem();
     CK(cudaFuncSetAttribute(k_eq_fused<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_xp_fused<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    CK(cudaFuncSetAttribute(k_eq_nttmac<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)k2_smem_bytes<LOGN>()));
-    CK(cudaFuncSetAttribute(k_xp_nttmac<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)k2_smem_bytes<LOGN>()));
     done = true;
     return 0;
   }
@@ -299,20 +362,20 @@ struct Engine {
         const int nn = (int)std::min(cn, nodes - n0);
         k_eq_dcp<LOGN, K, ELL><<<nn, T, 0, s>>>(state, (int)n0, k_aut, c->ws_dig.as<int>(), c->tb, c->cc, c->tc);
         CKL();
-        k_eq_nttmac<LOGN, K, ELL><<<nn * K, T, k2_smem_bytes<LOGN>(), s>>>(
+        k_eq_nttmac<LOGN, K, ELL><<<nn * K, T, 0, s>>>(
             state, C, (int)n0, c->ws_dig.as<int>(), ksk, k_aut, mono, out, Cout, c->tb, c->tc);
         CKL();
         *launches += 2;
       }
       return 0;
     }
-    const size_t per = (size_t)K * N + (size_t)ELL * N + (size_t)ELL * K * N;
+    const size_t per = (size_t)K * N + (size_t)ELL * N + (mode == 3 ? 0 : (size_t)ELL * K * N);
     const size_t chunk = op_chunk(per);
     const size_t nodes = (size_t)B * C;
     const size_t cn = std::min(chunk, nodes);
     if ((rc = c->ws_coeff.ensure(cn * K * N * 4))) return rc;
     if ((rc = c->ws_dig.ensure(cn * ELL * N * 4))) return rc;
-    if ((rc = c->ws_dn.ensure(cn * ELL * K * N * 4))) return rc;
+    if (mode != 3 && (rc = c->ws_dn.ensure(cn * ELL * K * N * 4))) return rc;
     for (size_t n0 = 0; n0 < nodes; n0 += cn) {
       const int nn = (int)std::min(cn, nodes - n0);
       k_op_eq_intt<LOGN, K><<<dim3(nn, K), T, 0, s>>>(state, (int)n0, k_aut, c->ws_coeff.as<u32>(), c->tb, c->tc);
@@ -321,7 +384,15 @@ struct Engine {
       k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), nn,
                                                                           c->ws_dig.as<int>(), c->tb, c->cc);
       CKL();
-      k_op_digit_ntt<LOGN, K><<<dim3(nn * ELL, K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(), c->tb, c->tc);
+      if (mode == 3) {  // hybrid: the digit NTTs stream straight into the key-switch MAC (K2)
+        k_eq_nttmac<LOGN, K, ELL><<<nn * K, T, 0, s>>>(state, C, (int)n0, c->ws_dig.as<int>(), ksk, k_aut, mono,
+                                                       out, Cout, c->tb, c->tc);
+        CKL();
+        *launches += 3;
+        continue;
+      }
+      k_op_digit_ntt<LOGN, K, ELL><<<dim3(nn * (ELL - 1), K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(), c->tb,
+                                                                        c->tc);
       CKL();
       const size_t tm = (size_t)nn * K * N;
       k_op_eq_mac<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(
@@ -353,7 +424,7 @@ struct Engine {
         const int nn = (int)std::min(cn, cts - m0);
         k_xp_dcp<LOGN, K, ELL><<<nn, T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_dig.as<int>(), c->tb, c->cc, c->tc);
         CKL();
-        k_xp_nttmac<LOGN, K, ELL><<<nn * K, T, k2_smem_bytes<LOGN>(), s>>>(in, in_b, M, (int)m0, pairs,
+        k_xp_nttmac<LOGN, K, ELL><<<nn * K, T, 0, s>>>(in, in_b, M, (int)m0, pairs,
                                                                          c->ws_dig.as<int>(), rows, out, out_b,
                                                                          c->tb, c->tc);
         CKL();
@@ -361,13 +432,13 @@ struct Engine {
       }
       return 0;
     }
-    const size_t per = 2 * ((size_t)K * N + (size_t)ELL * N + (size_t)ELL * K * N);
+    const size_t per = 2 * ((size_t)K * N + (size_t)ELL * N + (mode == 3 ? 0 : (size_t)ELL * K * N));
     const size_t chunk = op_chunk(per);
     const size_t cts = (size_t)B * M;
     const size_t cn = std::min(chunk, cts);
     if ((rc = c->ws_coeff.ensure(cn * 2 * K * N * 4))) return rc;
     if ((rc = c->ws_dig.ensure(cn * 2 * ELL * N * 4))) return rc;
-    if ((rc = c->ws_dn.ensure(cn * 2 * ELL * K * N * 4))) return rc;
+    if (mode != 3 && (rc = c->ws_dn.ensure(cn * 2 * ELL * K * N * 4))) return rc;
     for (size_t m0 = 0; m0 < cts; m0 += cn) {
       const int nn = (int)std::min(cn, cts - m0);
       k_op_xp_intt<LOGN, K><<<dim3(2 * nn, K), T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_coeff.as<u32>(), c->tb, c->tc);
@@ -376,7 +447,15 @@ struct Engine {
       k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), 2 * nn,
                                                                           c->ws_dig.as<int>(), c->tb, c->cc);
       CKL();
-      k_op_digit_ntt<LOGN, K><<<dim3(2 * nn * ELL, K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(), c->tb, c->tc);
+      if (mode == 3) {
+        k_xp_nttmac<LOGN, K, ELL><<<nn * K, T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_dig.as<int>(), rows, out,
+                                                       out_b, c->tb, c->tc);
+        CKL();
+        *launches += 3;
+        continue;
+      }
+      k_op_digit_ntt<LOGN, K, ELL><<<dim3(2 * nn * (ELL - 1), K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(),
+                                                                            c->tb, c->tc);
       CKL();
       const size_t tm = (size_t)nn * K * N;
       k_op_xp_mac<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(in, in_b, M, (int)m0, nn, pairs,
@@ -512,6 +591,29 @@ struct Engine {
     return r;
   }
 
+  // ColTor RGSW rows of bits [0, nb): a-digit rows from `arows` (query
+  // stride arows_b words, ELL rows per bit) and b-digit rows = the column
+  // leaves `cols` (query stride cols_b), folded (k_fold_rows) into ws_crows
+  // as (B, nb, 2 ELL) row groups.
+  static int fold_coltor(gpir_ctx* c, int B, uint32_t nb, const u32* arows, size_t arows_b, const u32* cols,
+                         size_t cols_b, cudaStream_t s) {
+    if (!nb) return 0;
+    u32* dst = c->ws_crows.as<u32>();
+    const size_t db = (size_t)nb * 2 * ELL * CT, dg = 2 * (size_t)ELL * CT;
+    int rc;
+    if ((rc = fold_rows(c, arows, dst, B, (int)nb, arows_b, (size_t)ELL * CT, db, dg, s))) return rc;
+    return fold_rows(c, cols, dst + (size_t)ELL * CT, B, (int)nb, cols_b, (size_t)ELL * CT, db, dg, s);
+  }
+  static RowsDesc coltor_rows(gpir_ctx* c, uint32_t nb, uint32_t j) {
+    RowsDesc r;
+    r.lo = c->ws_crows.as<u32>() + (size_t)j * 2 * ELL * CT;
+    r.lo_b = (size_t)nb * 2 * ELL * CT;
+    r.hi = r.lo + (size_t)ELL * CT;
+    r.hi_b = r.lo_b;
+    r.slot = nullptr;
+    return r;
+  }
+
   // expansion of B brv queries (in ws_state0 as (B,1)) -> leaves pointer (B, total)
   static int expand_all(gpir_ctx* c, int B, uint32_t total, const uint8_t* eq_modes, uint32_t n_eq,
                         const int* kslot, u32** leaves_out, cudaStream_t s, uint32_t* launches) {
@@ -524,18 +626,23 @@ struct Engine {
       const int mode = (eq_modes && t < n_eq) ? eq_modes[t] : default_mode(B * C);
       int rc = expand_stage(c, cur, B, C, nxt, Cout, (int)t, evk_rows(c, (int)t, kslot), mode, s, launches);
       if (rc) return rc;
+      g_sprof.mark(s, "eq" + std::to_string(t) + " " + "oFSH"[mode & 3]);
       std::swap(cur, nxt);
     }
     *leaves_out = cur;
     return 0;
   }
 
-  static int default_mode(size_t nodes) {
-    // B200 hybrid rule: the fused kernel runs one CTA (T threads, ~96 KiB smem) per
-    // node; below ~2 waves of 148 SMs x 2 CTAs the operation-level kernels (which
-    // expose ELL*K-fold more CTAs) win.
-    return nodes >= 2 * 148 * 2 ? 1 : 0;
-  }
+  // B200 hybrid rule (measured per stage at config 2, profiles/r1_plans.md):
+  // the operation-level kernels win while a stage has too few nodes to fill
+  // the GPU with one CTA per node x limb; beyond that the stage-level
+  // executor (mode 3: operation-level iNTT + Dcp feeding the fused digit-NTT
+  // + key-switch MAC kernel) is fastest.  The single-kernel node-fused
+  // executor (mode 1) is limited to 2 CTAs/SM by its 112 KiB of shared
+  // memory and is never the faster choice on B200.
+  static int eq_default(size_t nodes) { return nodes >= kEqStageNodes ? 3 : 0; }
+  static int xp_default(size_t cts) { return cts >= kXpStageCts ? 3 : 0; }
+  static int default_mode(size_t nodes) { return eq_default(nodes); }
 
   static int ensure_ws(gpir_ctx* c, int B, uint32_t total, uint32_t d1, uint32_t bits) {
     int rc;
@@ -547,6 +654,7 @@ struct Engine {
     if ((rc = c->ws_ct0.ensure((size_t)B * std::max<uint32_t>(d1 / 2, 1) * ctb))) return rc;
     if ((rc = c->ws_ct1.ensure((size_t)B * std::max<uint32_t>(d1 / 4, 1) * ctb))) return rc;
     if ((rc = c->ws_kslot.ensure((size_t)B * 4))) return rc;
+    if ((rc = c->ws_crows.ensure((size_t)B * std::max<uint32_t>(bits, 1) * 2 * ELL * ctb))) return rc;
     return 0;
   }
 
@@ -563,39 +671,42 @@ struct Engine {
     uint32_t launches = 0;
     int rc;
     if (st) CK(cudaEventRecord(c->ev[1], s));
+    g_sprof.mark(s, "start");
     u32* leaves = nullptr;
     if ((rc = expand_all(c, B, total, eq_modes, n_eq, kslot, &leaves, s, &launches))) return rc;
     if (st) CK(cudaEventRecord(c->ev[2], s));
     // RGSW assembly (src/protocol.py:383-409): a-rows = col_cts ⊡ RGSW(s)
     if (bits_tree > 0) {
       const int M = (int)(bits_tree * ELL);
-      const int mode = default_mode((size_t)B * M);
+      const int mode = xp_default((size_t)B * M);
       if ((rc = ext_product(c, leaves + (size_t)d0 * CT, total, B, M, 0, c->ws_arows.as<u32>(), (size_t)M,
                             skrgsw_rows(c, kslot), mode, s, &launches)))
         return rc;
     }
     if (st) CK(cudaEventRecord(c->ev[3], s));
+    g_sprof.mark(s, "rgsw");
     if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches,
                      st ? c->ev[11] : nullptr)))
       return rc;
     if (st) CK(cudaEventRecord(c->ev[4], s));
+    g_sprof.mark(s, "rowsel+pack");
     // ColTor (src/protocol.py:542-573): LSB-first pairs
+    if ((rc = fold_coltor(c, B, bits, c->ws_arows.as<u32>(), (size_t)bits_tree * ELL * CT, leaves + (size_t)d0 * CT,
+                          (size_t)total * CT, s)))
+      return rc;
     u32* cur = c->ws_sel.as<u32>();
     u32* bufs[2] = {c->ws_ct0.as<u32>(), c->ws_ct1.as<u32>()};
     for (uint32_t j = 0; j < bits; ++j) {
       const int C = (int)(d1 >> j);
-      RowsDesc r;
-      r.lo = c->ws_arows.as<u32>() + (size_t)j * ELL * CT;
-      r.lo_b = (size_t)bits_tree * ELL * CT;
-      r.hi = leaves + (size_t)(d0 + j * ELL) * CT;
-      r.hi_b = (size_t)total * CT;
-      r.slot = nullptr;
-      const int mode = (ct_modes && j < n_ct) ? ct_modes[j] : default_mode((size_t)B * C / 2);
+      const RowsDesc r = coltor_rows(c, bits, j);
+      const int mode = (ct_modes && j < n_ct) ? ct_modes[j] : xp_default((size_t)B * C / 2);
       u32* dst = bufs[j & 1];
       if ((rc = ext_product(c, cur, (size_t)C, B, C / 2, 1, dst, (size_t)C / 2, r, mode, s, &launches))) return rc;
+      g_sprof.mark(s, "coltor" + std::to_string(j) + " " + "oFSH"[mode & 3]);
       cur = dst;
     }
     if (st) CK(cudaEventRecord(c->ev[5], s));
+    g_sprof.flush();
     *result = cur;
     if (leaves_out) *leaves_out = leaves;
     if (st) st->launches += launches;
@@ -700,7 +811,7 @@ struct Engine {
     if (bits > 0) {
       const int M = (int)(bits * ELL);
       if ((rc = ext_product(c, leaves + (size_t)d0 * CT, total, B, M, 0, c->ws_arows.as<u32>(), (size_t)M,
-                            skrgsw_rows(c, c->ws_kslot.as<int>()), default_mode((size_t)B * M), s, &launches)))
+                            skrgsw_rows(c, c->ws_kslot.as<int>()), xp_default((size_t)B * M), s, &launches)))
         return rc;
     }
     CK(cudaMemcpy2DAsync(d_rows, (size_t)d0 * CT * 4, leaves, (size_t)total * CT * 4, (size_t)d0 * CT * 4, B,
@@ -725,16 +836,14 @@ struct Engine {
     u32* bufs[2] = {c->ws_ct0.as<u32>(), c->ws_ct1.as<u32>()};
     uint32_t launches = 0;
     int rc;
+    if ((rc = fold_coltor(c, B, bits, c->ws_arows.as<u32>(), (size_t)bits * ELL * CT, c->sh_leaves + (size_t)d0 * CT,
+                          (size_t)total * CT, s)))
+      return rc;
     for (uint32_t j = 0; j < bits; ++j) {
       const int C = (int)(d1 >> j);
-      RowsDesc r;
-      r.lo = c->ws_arows.as<u32>() + (size_t)j * ELL * CT;
-      r.lo_b = (size_t)bits * ELL * CT;
-      r.hi = c->sh_leaves + (size_t)(d0 + j * ELL) * CT;
-      r.hi_b = (size_t)total * CT;
-      r.slot = nullptr;
+      const RowsDesc r = coltor_rows(c, bits, j);
       u32* dst = bufs[j & 1];
-      if ((rc = ext_product(c, cur, (size_t)C, B, C / 2, 1, dst, (size_t)C / 2, r, default_mode((size_t)B * C / 2), s,
+      if ((rc = ext_product(c, cur, (size_t)C, B, C / 2, 1, dst, (size_t)C / 2, r, xp_default((size_t)B * C / 2), s,
                             &launches)))
         return rc;
       cur = dst;
@@ -754,6 +863,9 @@ struct Engine {
     if ((rc = bitrev_rows(c, d_cts, c->ws_state0.as<u32>(), (size_t)B * C * 2 * K, s))) return rc;
     if (bits) {
       if ((rc = bitrev_rows(c, d_rgsw, c->ws_io0.as<u32>(), (size_t)B * bits * 2 * ELL * 2 * K, s))) return rc;
+      if ((rc = fold_rows(c, c->ws_io0.as<u32>(), c->ws_io0.as<u32>(), B, (int)(2 * bits), (size_t)bits * 2 * ELL * CT,
+                          (size_t)ELL * CT, (size_t)bits * 2 * ELL * CT, (size_t)ELL * CT, s)))
+        return rc;
     }
     u32* cur = c->ws_state0.as<u32>();
     u32* bufs[2] = {c->ws_ct0.as<u32>(), c->ws_ct1.as<u32>()};
@@ -767,7 +879,7 @@ struct Engine {
       r.slot = nullptr;
       u32* dst = bufs[j & 1];
       if ((rc = ext_product(c, cur, (size_t)Cj, B, Cj / 2, 1, dst, (size_t)Cj / 2, r,
-                            default_mode((size_t)B * Cj / 2), s, &launches)))
+                            xp_default((size_t)B * Cj / 2), s, &launches)))
         return rc;
       cur = dst;
     }
@@ -858,6 +970,7 @@ int Engine<LOGN, K, ELL>::op_expand_stage(gpir_ctx* c, const u32* h_state, int B
   if ((rc = bitrev_rows(c, tmp.as<u32>(), st.as<u32>(), sw >> LOGN, s))) return rc;
   CK(cudaMemcpyAsync(tmp.p, h_ksk, kw * 4, cudaMemcpyHostToDevice, s));
   if ((rc = bitrev_rows(c, tmp.as<u32>(), ks.as<u32>(), kw >> LOGN, s))) return rc;
+  if ((rc = fold_rows(c, ks.as<u32>(), ks.as<u32>(), B, 1, (size_t)ELL * CT, 0, (size_t)ELL * CT, 0, s))) return rc;
   RowsDesc r;
   r.lo = ks.as<u32>();
   r.lo_b = (size_t)ELL * CT;
@@ -892,6 +1005,9 @@ int Engine<LOGN, K, ELL>::op_xp(gpir_ctx* c, const u32* h_cts, int B, int M, int
   if ((rc = bitrev_rows(c, tmp.as<u32>(), in.as<u32>(), iw >> LOGN, s))) return rc;
   CK(cudaMemcpyAsync(tmp.p, h_rows, rwn * 4, cudaMemcpyHostToDevice, s));
   if ((rc = bitrev_rows(c, tmp.as<u32>(), rw.as<u32>(), rwn >> LOGN, s))) return rc;
+  if ((rc = fold_rows(c, rw.as<u32>(), rw.as<u32>(), B, 2, 2 * (size_t)ELL * CT, (size_t)ELL * CT,
+                      2 * (size_t)ELL * CT, (size_t)ELL * CT, s)))
+    return rc;
   RowsDesc r;
   r.lo = rw.as<u32>();
   r.lo_b = 2 * (size_t)ELL * CT;
@@ -1169,16 +1285,17 @@ int gpir_keys_put(gpir_ctx* c, int slot, const uint32_t* evks, uint32_t stages, 
   if ((rc = tmp.ensure(std::max(ew, rw) * 4))) return rc;
   if (stages) {
     CK(cudaMemcpyAsync(tmp.p, evks, ew * 4, cudaMemcpyHostToDevice, c->stream));
-    if ((rc = bitrev_rows(c, tmp.as<u32>(), c->evk_pool.as<u32>() + (size_t)slot * c->key_stages * ell * CT,
-                          ew >> c->logn, c->stream)))
-      return rc;
+    u32* dst = c->evk_pool.as<u32>() + (size_t)slot * c->key_stages * ell * CT;
+    if ((rc = bitrev_rows(c, tmp.as<u32>(), dst, ew >> c->logn, c->stream))) return rc;
+    if ((rc = fold_rows(c, dst, dst, 1, (int)stages, 0, ell * CT, 0, ell * CT, c->stream))) return rc;
     CK(cudaStreamSynchronize(c->stream));
   }
   c->slot_rgsw[slot] = 0;
   if (sk_rgsw) {
     CK(cudaMemcpyAsync(tmp.p, sk_rgsw, rw * 4, cudaMemcpyHostToDevice, c->stream));
-    if ((rc = bitrev_rows(c, tmp.as<u32>(), c->rgsw_pool.as<u32>() + (size_t)slot * rw, rw >> c->logn, c->stream)))
-      return rc;
+    u32* dst = c->rgsw_pool.as<u32>() + (size_t)slot * rw;
+    if ((rc = bitrev_rows(c, tmp.as<u32>(), dst, rw >> c->logn, c->stream))) return rc;
+    if ((rc = fold_rows(c, dst, dst, 1, 2, 0, ell * CT, 0, ell * CT, c->stream))) return rc;
     CK(cudaStreamSynchronize(c->stream));
     c->slot_rgsw[slot] = 1;
   }
@@ -1260,10 +1377,9 @@ int gpir_plan(gpir_ctx* c, uint32_t d0, uint32_t d1, uint32_t B, uint8_t* eq_mod
   if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
   const uint32_t total = leaves_of(d0, d1, c->ell);
   const uint32_t st = stages_of(total), bits = ilog2(d1);
-  const size_t fill = 2 * 148 * 2;
   for (uint32_t t = 0; t < n_eq && t < st; ++t)
-    eq_modes[t] = (size_t)B * std::min<uint32_t>(1u << t, total) >= fill ? 1 : 0;
-  for (uint32_t j = 0; j < n_ct && j < bits; ++j) ct_modes[j] = (size_t)B * (d1 >> (j + 1)) >= fill ? 1 : 0;
+    eq_modes[t] = (size_t)B * std::min<uint32_t>(1u << t, total) >= kEqStageNodes ? 3 : 0;
+  for (uint32_t j = 0; j < n_ct && j < bits; ++j) ct_modes[j] = (size_t)B * (d1 >> (j + 1)) >= kXpStageCts ? 3 : 0;
   return 0;
 }
 

@@ -48,6 +48,12 @@ struct CrtConst {
   u64 dc_lo, dc_hi;                       // sum_{j < ell-1} (z/2 - 1) z^j (closed-form digits)
 };
 
+// Top-digit fold constants (see k_fold_rows): per limb i, w[i][j] = z^(j-(ell-1))
+// mod q_i for j < ell-1 and w[i][ell-1] = z^-(ell-1), with Shoup companions.
+struct FoldConst {
+  uint2 w[kMaxLimbs][kMaxEll];
+};
+
 // Device-resident transform tables for one context.
 struct Tables {
   const uint2* fwd;    // [k][n] (psi^brv(i), shoup)     forward CT twiddles

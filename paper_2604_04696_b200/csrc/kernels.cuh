@@ -257,6 +257,43 @@ constexpr int priv_slots() {
 }
 
 // ---------------------------------------------------------------------------
+// Top-digit fold of gadget key rows.  The gadget digits of a centered
+// coefficient satisfy sum_j z^j d_j = a_c exactly, so by linearity of the NTT
+//   NTT(d_{l-1}) = z^-(l-1) (A - sum_{j<l-1} z^j NTT(d_j))   (mod q_i)
+// with A = NTT(a) the (NTT-domain) input itself.  Hence for any key rows R_j
+//   sum_j NTT(d_j) R_j = sum_{j<l-1} NTT(d_j) R'_j + A R'_{l-1},
+//   R'_j = R_j - z^(j-(l-1)) R_{l-1},  R'_{l-1} = z^-(l-1) R_{l-1}.
+// The server folds every key row group once (evks and RGSW(s) at upload, the
+// ColTor RGSW rows when they are assembled) and then transforms only l-1
+// digits per component: one forward NTT in every five is replaced by a MAC
+// of the input.  Exact modular arithmetic, so bit-identical results.
+// One thread per (b, group, word); src may alias dst.
+template <int ELL>
+__global__ void k_fold_rows(const u32* src, u32* dst, int B, int G, size_t sb, size_t sg, size_t db, size_t dg,
+                            int logn, int K, Tables tb, FoldConst fc) {
+  const size_t CTW = (size_t)2 * K << logn;
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (size_t)B * G * CTW) return;
+  const size_t w = g % CTW, bg = g / CTW;
+  const int grp = (int)(bg % G), b = (int)(bg / G);
+  const int i = (int)((w >> logn) % K);
+  const u32 q = tb.mod[i].q;
+  const u32* s = src + b * sb + grp * sg + w;
+  u32* d = dst + b * db + grp * dg + w;
+  u32 r[ELL];
+#pragma unroll
+  for (int j = 0; j < ELL; ++j) r[j] = s[(size_t)j * CTW];
+  const u32 top = r[ELL - 1];
+#pragma unroll
+  for (int j = 0; j < ELL - 1; ++j) {
+    const uint2 c = fc.w[i][j];
+    d[(size_t)j * CTW] = mod_sub(r[j], csub(mul_shoup(top, c.x, c.y, q), q), q);
+  }
+  const uint2 c = fc.w[i][ELL - 1];
+  d[(size_t)(ELL - 1) * CTW] = csub(mul_shoup(top, c.x, c.y, q), q);
+}
+
+// ---------------------------------------------------------------------------
 // Stage-fused ExpandQuery node (expand_stage STAGE_LEVEL, src/planner.py:364-380):
 // one CTA per tree node.  Automorphism gather + iNTT of `a` for all limbs,
 // Dcp, then per output limb: ELL digit NTTs, key-switch MAC against the
@@ -315,6 +352,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
     const Modulus M = tb.mod[i];
     const u32 q = M.q;
     const u32 qinv = 0u - M.qinv_neg;
+    const u32* sta = st + (size_t)i * N;
     const u32* stb = st + (size_t)(K + i) * N;
     u32 gb[16];
     int acc0[16], acc1[16];
@@ -326,7 +364,14 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
       Key16 ka, kb;
       ka.load(ra + i0);
       kb.load(ra + (size_t)K * N + i0);
-      if (j == ELL - 1) {  // the automorphism gather of b for the combine, in flight during the last transform
+      if (j == ELL - 1) {  // top digit folded into the keys: MAC the automorphed input tau(a) directly
+        u32 x[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) x[r] = __ldg(sta + aut_src(i0 + r, k_aut, LOGN));
+        mont_mac16(x, ka, kb, acc0, acc1, q, qinv);
+        break;
+      }
+      if (j == ELL - 2) {  // the automorphism gather of b for the combine, in flight during the last transform
 #pragma unroll
         for (int r = 0; r < 16; ++r) gb[r] = __ldg(stb + aut_src(i0 + r, k_aut, LOGN));
       }
@@ -415,6 +460,19 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
         Key16 ka, kb;
         ka.load(ra + i0);
         kb.load(ra + (size_t)K * N + i0);
+        if (j == ELL - 1) {  // folded top digit: MAC this component of the input directly
+          const size_t off = (size_t)(comp * K + i) * N + i0;
+          u32 x[16];
+          ld16(src + off, x);
+          if (pairs) {
+            u32 o[16];
+            ld16(odd + off, o);
+#pragma unroll
+            for (int r = 0; r < 16; ++r) x[r] = mod_sub(o[r], x[r], q);
+          }
+          mont_mac16(x, ka, kb, acc0, acc1, q, qinv);
+          break;
+        }
         ntt_fwd<LOGN, true>(
             ns, tb.fwd + (size_t)i * N, tc.f[i], Mi, [&](int jj) -> u32 { return lift(priv[pv<T>(j, jj >> SH)], q); },
             [&](int, const u32(&x)[16]) { mont_mac16(x, ka, kb, acc0, acc1, q, qinv); });
@@ -524,14 +582,15 @@ __global__ void k_op_dcp(const u32* __restrict__ coeff, int polys, int* __restri
   for (int e = 0; e < ELL; ++e) digits[(p * ELL + e) * N + j] = d[e];
 }
 
-// (3) digit NTT: grid (polys*ELL, K): lift digit mod q_i, forward NTT.
-template <int LOGN, int K>
+// (3) digit NTT: grid (polys*(ELL-1), K): lift digit mod q_i, forward NTT
+// (the top digit is folded into the keys, k_fold_rows).
+template <int LOGN, int K, int ELL>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T)
     k_op_digit_ntt(const int* __restrict__ digits, u32* __restrict__ dn, Tables tb, const __grid_constant__ TwConst tc) {
   constexpr int N = 1 << LOGN;
   __shared__ __align__(16) u32 xbuf[2 * N];
   NttState ns{xbuf, 0};
-  const int pe = blockIdx.x, i = blockIdx.y;
+  const int pe = (blockIdx.x / (ELL - 1)) * ELL + blockIdx.x % (ELL - 1), i = blockIdx.y;
   const int* src = digits + (size_t)pe * N;
   const u32 q = tb.mod[i].q;
   u32* dst = dn + ((size_t)pe * K + i) * N;
@@ -556,15 +615,16 @@ __global__ void k_op_eq_mac(const u32* __restrict__ state, int C, int node0, int
   const size_t CT = 2 * (size_t)K * N;
   const Modulus M = tb.mod[i];
   const u32 q = M.q;
+  const u32* st = state + (size_t)gn * CT;
   u64 a0 = 0, a1 = 0;
 #pragma unroll
-  for (int j = 0; j < ELL; ++j) {
-    const u32 d = __ldg(dn + (((size_t)nd * ELL + j) * K + i) * N + pos);
+  for (int j = 0; j < ELL; ++j) {  // digit ELL-1 is folded: its term is tau(a) itself
+    const u32 d = j < ELL - 1 ? __ldg(dn + (((size_t)nd * ELL + j) * K + i) * N + pos)
+                              : __ldg(st + (size_t)i * N + aut_src(pos, k_aut, LOGN));
     const u32* ra = ksk.row(b, j, ELL, CT) + (size_t)i * N + pos;
     a0 += (u64)d * __ldg(ra);
     a1 += (u64)d * __ldg(ra + (size_t)K * N);
   }
-  const u32* st = state + (size_t)gn * CT;
   const u32 ca = __ldg(st + (size_t)i * N + pos), cb = __ldg(st + (size_t)(K + i) * N + pos);
   const u32 sa = reduce_u64(a0, M);
   const u32 sb = mod_add(reduce_u64(a1, M), __ldg(st + (size_t)(K + i) * N + aut_src(pos, k_aut, LOGN)), q);
@@ -594,12 +654,20 @@ __global__ void k_op_xp_mac(const u32* __restrict__ in, size_t in_b, int M_per_b
   const size_t CT = 2 * (size_t)K * N;
   const Modulus M = tb.mod[i];
   const u32 q = M.q;
+  const u32* src = pairs ? in + (b * in_b + 2 * (size_t)m) * CT : in + (b * in_b + (size_t)m) * CT;
   u64 a0 = 0, a1 = 0;
 #pragma unroll
   for (int comp = 0; comp < 2; ++comp) {
 #pragma unroll
     for (int j = 0; j < ELL; ++j) {
-      const u32 d = __ldg(dn + ((((size_t)ct * 2 + comp) * ELL + j) * K + i) * N + pos);
+      u32 d;
+      if (j < ELL - 1) {
+        d = __ldg(dn + ((((size_t)ct * 2 + comp) * ELL + j) * K + i) * N + pos);
+      } else {  // folded top digit: this component of the input (or odd - even)
+        const size_t off = (size_t)(comp * K + i) * N + pos;
+        d = __ldg(src + off);
+        if (pairs) d = mod_sub(__ldg(src + CT + off), d, q);
+      }
       const u32* ra = rows.row(b, comp * ELL + j, ELL, CT) + (size_t)i * N + pos;
       a0 += (u64)d * __ldg(ra);
       a1 += (u64)d * __ldg(ra + (size_t)K * N);

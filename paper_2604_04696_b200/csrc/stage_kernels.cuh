@@ -10,27 +10,20 @@
 //      then the exact CRT + centered digit extraction in registers; the signed
 //      digits (int32, natural coefficient order) go to a per-stage scratch.
 //   K2 (one CTA per node x output limb): for every digit, lift mod q_limb,
-//      forward NTT and accumulate digit * key-row for both ciphertext
-//      components in 64-bit registers; the two key rows of the next digit
-//      are prefetched into shared memory with cp.async.bulk on an mbarrier
-//      while the current digit is transformed; the epilogue applies the
-//      combine of the phase and writes the output limb.
+//      lazy forward NTT and a 32-bit Montgomery MAC of digit * key-row for
+//      both ciphertext components (key rows fetched at the start of each
+//      transform); the epilogue applies the combine of the phase and writes
+//      the output limb.
 //
 // Compared with one CTA per node (which needs 112 KiB of shared memory for
-// the digits and exchange buffers) K2 uses 96 KiB with the key double
-// buffer, exposes K-fold more CTAs per stage, and never waits on an L2 key
-// load inside the MAC.
+// the digits and exchange buffers, two CTAs per SM) K2 needs only the 32 KiB
+// exchange buffer and <= 85 registers, so three CTAs run per SM, and it
+// exposes K-fold more CTAs per stage.
 #pragma once
 #include "kernels.cuh"
 #include "rowsel_tc.cuh"
 
 namespace gpir {
-
-// K2 shared memory: xbuf (2N words) + keys [2 buffers][2 comps][N words] + 2 mbarriers
-template <int LOGN>
-constexpr size_t k2_smem_bytes() {
-  return (size_t)NttCfg<LOGN>::XBUF_WORDS * 4 + (size_t)4 * (1 << LOGN) * 4 + 2 * 8;
-}
 
 // ---------------------------------------------------------------------------
 // K1, ExpandQuery: a-component of node (node0 + blockIdx.x), automorphism
@@ -123,166 +116,172 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
 }
 
 // ---------------------------------------------------------------------------
-// K2 core: acc{0,1} = sum_{j < NDIG} NTT_i(digit j) * row_j[comp][limb i],
-// row_j = rows(j) (a comp; b comp at + K*N).  Key rows of digit j+1 are
-// prefetched into smem while digit j is transformed.
-template <int LOGN, int K, class RowFn>
-__device__ __forceinline__ void k2_mac(NttState& ns, u32* keys, uint64_t* kbar, const int* __restrict__ dig, int ndig,
-                                       int i, RowFn&& row, const Tables& tb, const TwConst& tc, Acc (&acc0)[16],
-                                       Acc (&acc1)[16]) {
-  constexpr int N = 1 << LOGN, SH = NttCfg<LOGN>::SHIFT;
+// K2 core: acc{0,1} = sum_{j < NDIG} NTT_i(digit j) * row_j[comp][limb i] * 2^-32
+// (mont_mac on lazy transform outputs), row_j = rows(j) (a comp; b comp at
+// + K*N).  Shared memory is just the exchange buffer and the accumulators are
+// 32-bit, so three CTAs fit per SM; the key rows of digit j are issued at the
+// start of its transform and land while the butterflies run.
+// Digits come in groups of ELL (one group per input component, `groups` of
+// them); the top digit of each group is folded into its key row
+// (k_fold_rows), so its term is direct(group, quarter, x) -- the component's
+// NTT-domain input -- instead of a transform.
+template <int LOGN, int K, int ELL, class RowFn, class DirFn>
+__device__ __forceinline__ void k2_mac(NttState& ns, const int* __restrict__ dig, int groups, int i, RowFn&& row,
+                                       DirFn&& direct, const Tables& tb, const TwConst& tc, int (&acc0)[16],
+                                       int (&acc1)[16]) {
+  constexpr int N = 1 << LOGN;
   const int tid = threadIdx.x;
   const Modulus& Mi = tb.mod[i];
-  const u32 q = Mi.q;
+  const u32 q = Mi.q, qinv = 0u - Mi.qinv_neg;
   const int i0 = tid << 4;
-  auto prefetch = [&](int j) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads before async writes
-    const u32* ra = row(j) + (size_t)i * N;
-    u32* kb = keys + (size_t)(j & 1) * 2 * N;
-    mbar_expect_tx(&kbar[j & 1], 2 * N * 4);
-    bulk_g2s(kb, ra, N * 4, &kbar[j & 1]);
-    bulk_g2s(kb + N, ra + (size_t)K * N, N * 4, &kbar[j & 1]);
-  };
-  if (tid == 0) prefetch(0);
 #pragma unroll
-  for (int r = 0; r < 16; ++r) acc_zero(acc0[r]), acc_zero(acc1[r]);
+  for (int r = 0; r < 16; ++r) acc0[r] = acc1[r] = 0;
 #pragma unroll 1
-  for (int j = 0; j < ndig; ++j) {
-    __syncthreads();  // every thread is past the MAC of digit j-1: its key buffer may be refilled
-    if (tid == 0 && j + 1 < ndig) prefetch(j + 1);
-    const int* dj = dig + (size_t)j * N;
-    ntt_fwd<LOGN>(
-        ns, tb.fwd + (size_t)i * N, tc.f[i], Mi, [&](int jj) -> u32 { return lift(__ldg(dj + jj), q); },
-        [&](int, const u32(&x)[16]) {
-          mbar_wait(&kbar[j & 1], (j >> 1) & 1);
-          const u32* ka = keys + (size_t)(j & 1) * 2 * N + i0;
-          const u32* kb = ka + N;
+  for (int g = 0; g < groups; ++g) {
+#pragma unroll 1
+    for (int j = g * ELL; j < g * ELL + ELL - 1; ++j) {
+      const int* dj = dig + (size_t)j * N;
+      const u32* ra = row(j) + (size_t)i * N + i0;
+      Key16 ka, kb;
+      ka.load(ra);
+      kb.load(ra + (size_t)K * N);
+      ntt_fwd<LOGN, true>(
+          ns, tb.fwd + (size_t)i * N, tc.f[i], Mi, [&](int jj) -> u32 { return lift(__ldg(dj + jj), q); },
+          [&](int, const u32(&x)[16]) { mont_mac16(x, ka, kb, acc0, acc1, q, qinv); });
+    }
+    const u32* ra = row(g * ELL + ELL - 1) + (size_t)i * N + i0;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint4 a = *reinterpret_cast<const uint4*>(ka + 4 * c);
-            const uint4 b = *reinterpret_cast<const uint4*>(kb + 4 * c);
-            acc_mac(acc0[4 * c], x[4 * c], a.x);
-            acc_mac(acc0[4 * c + 1], x[4 * c + 1], a.y);
-            acc_mac(acc0[4 * c + 2], x[4 * c + 2], a.z);
-            acc_mac(acc0[4 * c + 3], x[4 * c + 3], a.w);
-            acc_mac(acc1[4 * c], x[4 * c], b.x);
-            acc_mac(acc1[4 * c + 1], x[4 * c + 1], b.y);
-            acc_mac(acc1[4 * c + 2], x[4 * c + 2], b.z);
-            acc_mac(acc1[4 * c + 3], x[4 * c + 3], b.w);
-          }
-        });
+    for (int h = 0; h < 4; ++h) {  // in quarters of 4 slots: few live registers
+      const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(ra) + h);
+      const uint4 b4 = __ldg(reinterpret_cast<const uint4*>(ra + (size_t)K * N) + h);
+      u32 x[4];
+      direct(g, h, x);
+      const u32 av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        mont_mac(acc0[4 * h + rr], x[rr], av[rr], q, qinv);
+        mont_mac(acc1[4 * h + rr], x[rr], bv[rr], q, qinv);
+      }
+    }
   }
-  (void)SH;
 }
 
-template <int LOGN>
-__device__ __forceinline__ void k2_init(u32* smem, NttState& ns, u32*& keys, uint64_t*& kbar) {
-  constexpr int N = 1 << LOGN;
-  ns.xbuf = smem;
-  ns.parity = 0;
-  keys = smem + NttCfg<LOGN>::XBUF_WORDS;
-  kbar = reinterpret_cast<uint64_t*>(keys + 4 * N);
-  if (threadIdx.x == 0) {
-    mbar_init(&kbar[0], 1);
-    mbar_init(&kbar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-}
+#ifndef K2_MINB
+#define K2_MINB 3
+#endif
 
 // K2, ExpandQuery: node (node0 + blockIdx.x / K), output limb blockIdx.x % K
 template <int LOGN, int K, int ELL>
-__global__ void __launch_bounds__(NttCfg<LOGN>::T, 2)
+__global__ void __launch_bounds__(NttCfg<LOGN>::T, K2_MINB)
     k_eq_nttmac(const u32* __restrict__ state, int C, int node0, const int* __restrict__ dig, RowsDesc ksk, u32 k_aut,
                 const uint2* __restrict__ mono, u32* __restrict__ out, int Cout, Tables tb,
                 const __grid_constant__ TwConst tc) {
   constexpr int N = 1 << LOGN;
-  extern __shared__ __align__(128) u32 smem[];
-  NttState ns;
-  u32* keys;
-  uint64_t* kbar;
-  k2_init<LOGN>(smem, ns, keys, kbar);
+  __shared__ __align__(16) u32 xbuf[NttCfg<LOGN>::XBUF_WORDS];
+  NttState ns{xbuf, 0};
   const int tid = threadIdx.x;
   const int ln = blockIdx.x / K, i = blockIdx.x % K;
   const int gn = node0 + ln;
   const int b = gn / C, c = gn % C;
   const size_t CT = 2 * (size_t)K * N;
-  Acc acc0[16], acc1[16];
-  k2_mac<LOGN, K>(ns, keys, kbar, dig + (size_t)ln * ELL * N, ELL, i,
-                  [&](int j) { return ksk.row(b, j, ELL, CT); }, tb, tc, acc0, acc1);
+  int acc0[16], acc1[16];
+  const u32* sta = state + (size_t)gn * CT + (size_t)i * N;
+  k2_mac<LOGN, K, ELL>(
+      ns, dig + (size_t)ln * ELL * N, 1, i, [&](int j) { return ksk.row(b, j, ELL, CT); },
+      [&](int, int h, u32(&x)[4]) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) x[r] = __ldg(sta + aut_src((tid << 4) + 4 * h + r, k_aut, LOGN));
+      },
+      tb, tc, acc0, acc1);
   // combine (src/planner.py:361-363): out[c] = state + s, out[c + C] = X^-2^t (state - s)
   const Modulus M = tb.mod[i];
   const u32 q = M.q;
   const int i0 = tid << 4;
   const u32* st = state + (size_t)gn * CT;
-  u32 ca[16], cb[16];
-  ld16(st + (size_t)i * N + i0, ca);
-  ld16(st + (size_t)(K + i) * N + i0, cb);
   const u32* stb = st + (size_t)(K + i) * N;
-  u32 xa[16], xb[16], ya[16], yb[16];
-#pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const u32 sa = reduce_acc(acc0[r], M);
-    const u32 sb = mod_add(reduce_acc(acc1[r], M), __ldg(stb + aut_src(i0 + r, k_aut, LOGN)), q);
-    xa[r] = mod_add(ca[r], sa, q);
-    xb[r] = mod_add(cb[r], sb, q);
-    const uint2 w = __ldg(&mono[(size_t)i * N + i0 + r]);
-    ya[r] = csub(mul_shoup(mod_sub(ca[r], sa, q), w.x, w.y, q), q);
-    yb[r] = csub(mul_shoup(mod_sub(cb[r], sb, q), w.x, w.y, q), q);
-  }
   u32* o0 = out + ((size_t)b * Cout + c) * CT;
-  st16(o0 + (size_t)i * N + i0, xa);
-  st16(o0 + (size_t)(K + i) * N + i0, xb);
-  if (c + C < Cout) {
-    u32* o1 = out + ((size_t)b * Cout + c + C) * CT;
-    st16(o1 + (size_t)i * N + i0, ya);
-    st16(o1 + (size_t)(K + i) * N + i0, yb);
+  u32* o1 = out + ((size_t)b * Cout + c + C) * CT;
+  const bool second = c + C < Cout;
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {  // four quarters of 4 slots: few live registers
+    const uint4 ca = __ldg(reinterpret_cast<const uint4*>(st + (size_t)i * N + i0) + h);
+    const uint4 cb = __ldg(reinterpret_cast<const uint4*>(stb + i0) + h);
+    const u32 cav[4] = {ca.x, ca.y, ca.z, ca.w}, cbv[4] = {cb.x, cb.y, cb.z, cb.w};
+    u32 xa[4], xb[4], ya[4], yb[4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const int r = 4 * h + rr;
+      const u32 sa = mont_fin(acc0[r], ELL, M);
+      const u32 sb = mod_add(mont_fin(acc1[r], ELL, M), __ldg(stb + aut_src(i0 + r, k_aut, LOGN)), q);
+      xa[rr] = mod_add(cav[rr], sa, q);
+      xb[rr] = mod_add(cbv[rr], sb, q);
+      const uint2 w = __ldg(&mono[(size_t)i * N + i0 + r]);
+      ya[rr] = csub(mul_shoup(mod_sub(cav[rr], sa, q), w.x, w.y, q), q);
+      yb[rr] = csub(mul_shoup(mod_sub(cbv[rr], sb, q), w.x, w.y, q), q);
+    }
+    reinterpret_cast<uint4*>(o0 + (size_t)i * N + i0)[h] = make_uint4(xa[0], xa[1], xa[2], xa[3]);
+    reinterpret_cast<uint4*>(o0 + (size_t)(K + i) * N + i0)[h] = make_uint4(xb[0], xb[1], xb[2], xb[3]);
+    if (second) {
+      reinterpret_cast<uint4*>(o1 + (size_t)i * N + i0)[h] = make_uint4(ya[0], ya[1], ya[2], ya[3]);
+      reinterpret_cast<uint4*>(o1 + (size_t)(K + i) * N + i0)[h] = make_uint4(yb[0], yb[1], yb[2], yb[3]);
+    }
   }
 }
 
 // K2, external product / ColTor: ct (m0 + blockIdx.x / K), output limb blockIdx.x % K
 template <int LOGN, int K, int ELL>
-__global__ void __launch_bounds__(NttCfg<LOGN>::T, 2)
+__global__ void __launch_bounds__(NttCfg<LOGN>::T, K2_MINB)
     k_xp_nttmac(const u32* __restrict__ in, size_t in_b, int M_per_b, int m0, int pairs, const int* __restrict__ dig,
                 RowsDesc rows, u32* __restrict__ out, size_t out_b, Tables tb, const __grid_constant__ TwConst tc) {
   constexpr int N = 1 << LOGN;
-  extern __shared__ __align__(128) u32 smem[];
-  NttState ns;
-  u32* keys;
-  uint64_t* kbar;
-  k2_init<LOGN>(smem, ns, keys, kbar);
+  __shared__ __align__(16) u32 xbuf[NttCfg<LOGN>::XBUF_WORDS];
+  NttState ns{xbuf, 0};
   const int tid = threadIdx.x;
   const int lc = blockIdx.x / K, i = blockIdx.x % K;
   const int g = m0 + lc;
   const int b = g / M_per_b, m = g % M_per_b;
   const size_t CT = 2 * (size_t)K * N;
-  Acc acc0[16], acc1[16];
+  int acc0[16], acc1[16];
+  const u32* src = pairs ? in + (b * in_b + 2 * (size_t)m) * CT : in + (b * in_b + (size_t)m) * CT;
   // digits: a-component's ELL then b-component's ELL, matching rows [0, 2 ELL)
-  k2_mac<LOGN, K>(ns, keys, kbar, dig + (size_t)lc * 2 * ELL * N, 2 * ELL, i,
-                  [&](int j) { return rows.row(b, j, ELL, CT); }, tb, tc, acc0, acc1);
+  k2_mac<LOGN, K, ELL>(
+      ns, dig + (size_t)lc * 2 * ELL * N, 2, i, [&](int j) { return rows.row(b, j, ELL, CT); },
+      [&](int comp, int h, u32(&x)[4]) {
+        const size_t off = (size_t)(comp * K + i) * N + (tid << 4) + 4 * h;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + off));
+        x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+        if (pairs) {
+          const uint4 o = __ldg(reinterpret_cast<const uint4*>(src + CT + off));
+          const u32 q = tb.mod[i].q;
+          x[0] = mod_sub(o.x, x[0], q), x[1] = mod_sub(o.y, x[1], q), x[2] = mod_sub(o.z, x[2], q),
+          x[3] = mod_sub(o.w, x[3], q);
+        }
+      },
+      tb, tc, acc0, acc1);
   const Modulus M = tb.mod[i];
   const u32 q = M.q;
   const int i0 = tid << 4;
-  u32 sa[16], sb[16];
-#pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    sa[r] = reduce_acc(acc0[r], M);
-    sb[r] = reduce_acc(acc1[r], M);
-  }
-  if (pairs) {  // coltor_stage: even + (odd - even) ⊡ rgsw (src/planner.py:457-463)
-    const u32* ev = in + (b * in_b + 2 * (size_t)m) * CT;
-    u32 ea[16], eb[16];
-    ld16(ev + (size_t)i * N + i0, ea);
-    ld16(ev + (size_t)(K + i) * N + i0, eb);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      sa[r] = mod_add(sa[r], ea[r], q);
-      sb[r] = mod_add(sb[r], eb[r], q);
-    }
-  }
+  const u32* ev = in + (b * in_b + 2 * (size_t)m) * CT;  // ColTor: even + (odd - even) ⊡ rgsw (src/planner.py:457-463)
   u32* d = out + (b * out_b + (size_t)m) * CT;
-  st16(d + (size_t)i * N + i0, sa);
-  st16(d + (size_t)(K + i) * N + i0, sb);
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    u32 sa[4], sb[4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      sa[rr] = mont_fin(acc0[4 * h + rr], 2 * ELL, M);
+      sb[rr] = mont_fin(acc1[4 * h + rr], 2 * ELL, M);
+    }
+    if (pairs) {
+      const uint4 ea = __ldg(reinterpret_cast<const uint4*>(ev + (size_t)i * N + i0) + h);
+      const uint4 eb = __ldg(reinterpret_cast<const uint4*>(ev + (size_t)(K + i) * N + i0) + h);
+      sa[0] = mod_add(sa[0], ea.x, q); sa[1] = mod_add(sa[1], ea.y, q);
+      sa[2] = mod_add(sa[2], ea.z, q); sa[3] = mod_add(sa[3], ea.w, q);
+      sb[0] = mod_add(sb[0], eb.x, q); sb[1] = mod_add(sb[1], eb.y, q);
+      sb[2] = mod_add(sb[2], eb.z, q); sb[3] = mod_add(sb[3], eb.w, q);
+    }
+    reinterpret_cast<uint4*>(d + (size_t)i * N + i0)[h] = make_uint4(sa[0], sa[1], sa[2], sa[3]);
+    reinterpret_cast<uint4*>(d + (size_t)(K + i) * N + i0)[h] = make_uint4(sb[0], sb[1], sb[2], sb[3]);
+  }
 }
 
 }  // namespace gpir

@@ -39,9 +39,9 @@ def _u32(a):
 
 
 def _mode(mode) -> int:
-    """ExecMode / 'op' / 'stage' / 'split' -> C-ABI mode code (include/gpir.h)."""
+    """ExecMode / 'op' / 'stage' / 'split' / 'hybrid' -> C-ABI mode code (include/gpir.h)."""
     v = getattr(mode, "value", mode)
-    return {"op": 0, 0: 0, "stage": 1, 1: 1, "split": 2, 2: 2}[v]
+    return {"op": 0, 0: 0, "stage": 1, 1: 1, "split": 2, 2: 2, "hybrid": 3, 3: 3}[v]
 
 
 def ntt_raw(x, basis, gadget=None):

@@ -135,9 +135,17 @@ def choose_mode(working_set_bytes: int, hw: HardwareModel) -> ExecMode:
     return ExecMode.STAGE_LEVEL if working_set_bytes >= hw.l2_bytes else ExecMode.OPERATION_LEVEL
 
 
-def choose_mode_occupancy(nodes_in_batch: int, hw: HardwareModel) -> ExecMode:
-    """B200 rule: fuse once the stage has >= 2 waves of one-CTA-per-node work."""
-    fill = 2 * hw.processors * hw.resident_ctas
+# B200 thresholds of the occupancy rule, measured per stage at config 2
+# (profiles/r1_plans.md); identical to kEqStageNodes / kXpStageCts in gpir.cu
+EQ_STAGE_NODES = 2048
+XP_STAGE_CTS = 256
+
+
+def choose_mode_occupancy(nodes_in_batch: int, hw: HardwareModel, phase: "Phase | None" = None) -> ExecMode:
+    """B200 rule: run a stage on the stage-level executor once it has enough
+    nodes (ExpandQuery) or ciphertexts (ColTor) to fill the GPU with one CTA
+    per node x limb; the operation-level kernels win below that."""
+    fill = XP_STAGE_CTS if phase is Phase.COL_TOR else EQ_STAGE_NODES
     return ExecMode.STAGE_LEVEL if nodes_in_batch >= fill else ExecMode.OPERATION_LEVEL
 
 
@@ -151,7 +159,8 @@ def build_plan(config, params, batch: int, hw: HardwareModel | None = None, rule
     for t in range(num_expand_stages(total)):
         ws = working_set(Phase.EXPAND_QUERY, t, batch, params, config)
         nodes = expand_nodes(total, t)
-        mode = choose_mode(ws, hw) if rule == "working_set" else choose_mode_occupancy(nodes * batch, hw)
+        mode = choose_mode(ws, hw) if rule == "working_set" else choose_mode_occupancy(nodes * batch, hw,
+                                                                                         Phase.EXPAND_QUERY)
         if mode is ExecMode.STAGE_LEVEL and et is None:
             et = t
         expand.append(StageProfile(Phase.EXPAND_QUERY, t, nodes, _poly_bytes(params), batch, ws, mode))
@@ -159,7 +168,8 @@ def build_plan(config, params, batch: int, hw: HardwareModel | None = None, rule
     for t in range(num_coltor_stages(config.d1)):
         ws = working_set(Phase.COL_TOR, t, batch, params, config)
         nodes = coltor_nodes(config.d1, t)
-        mode = choose_mode(ws, hw) if rule == "working_set" else choose_mode_occupancy(nodes * batch, hw)
+        mode = choose_mode(ws, hw) if rule == "working_set" else choose_mode_occupancy(nodes * batch, hw,
+                                                                                         Phase.COL_TOR)
         if mode is ExecMode.STAGE_LEVEL:
             saw = True
         elif saw and ct is None:

@@ -321,16 +321,22 @@ _ENGINES = {"auto": 0, "cuda": 0, "transposed": 0, "pipeline": 0, "pmajor": 1, "
             "tensorcore": 2}
 
 
+STAGE_CODE = 3
+
+
 def _modes(config, params, B, hw, plan, mode):
     ell = params.gadget.ell
     total = planner.expansion_leaves(config.d0, config.d1, ell)
     ne, nc = planner.num_expand_stages(total), planner.num_coltor_stages(config.d1)
+    # STAGE_LEVEL runs B200's stage-level executor (C-ABI mode 3: the digit
+    # NTTs stream straight into the key-switch MAC, no materialised digit
+    # NTTs), OPERATION_LEVEL the per-primitive kernels (mode 0)
     if mode is not None:
-        v = 1 if mode is ExecMode.STAGE_LEVEL or getattr(mode, "value", None) == "stage" else 0
+        v = STAGE_CODE if mode is ExecMode.STAGE_LEVEL or getattr(mode, "value", None) == "stage" else 0
         return np.full(max(ne, 1), v, np.uint8), np.full(max(nc, 1), v, np.uint8)
     if plan is None:
         plan = planner.build_plan(config, params, B, hw if hw is not None else HardwareModel.b200())
-    fused = lambda m: 1 if getattr(m, "value", m) == "stage" else 0
+    fused = lambda m: STAGE_CODE if getattr(m, "value", m) == "stage" else 0
     em = np.array([fused(plan.mode_for(Phase.EXPAND_QUERY, t)) for t in range(ne)] or [0], np.uint8)
     cm = np.array([fused(plan.mode_for(Phase.COL_TOR, t)) for t in range(nc)] or [0], np.uint8)
     return em, cm

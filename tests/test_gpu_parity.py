@@ -78,7 +78,7 @@ def test_digits_extremes(G, tag):
 
 
 @pytest.mark.parametrize("tag", list(PROFILES))
-@pytest.mark.parametrize("mode", ["op", "stage", "split"])
+@pytest.mark.parametrize("mode", ["op", "stage", "split", "hybrid"])
 def test_subs_and_external_product_golden(G, golden, tag, mode):
     from paper_2604_04696_b200 import ops
     _, vec = golden
@@ -92,7 +92,7 @@ def test_subs_and_external_product_golden(G, golden, tag, mode):
     assert np.array_equal(xp, vec[f"{tag}_xp_out"])
 
 
-@pytest.mark.parametrize("mode", ["op", "stage", "split"])
+@pytest.mark.parametrize("mode", ["op", "stage", "split", "hybrid"])
 def test_expand_stages_and_coltor_vs_oracle(G, mode):
     from paper_2604_04696_b200 import ops
     po = O.default_params()

@@ -84,7 +84,9 @@ def test_planner_laws():
     assert ws == 5_368_709_120
     plan = G.build_plan(G.DbConfig(256, 64, 8192), p, 32, G.HardwareModel.b200())
     modes = "".join("F" if s.mode is G.ExecMode.STAGE_LEVEL else "o" for s in plan.expand_stages)
-    assert modes == "oooooFFFF"   # fused once B*nodes >= 2 waves of 148 SMs x 2 CTAs
+    assert modes == "ooooooFFF"   # stage-level once B * nodes >= 2048 (measured crossover, profiles/r1_plans.md)
+    cmodes = "".join("F" if s.mode is G.ExecMode.STAGE_LEVEL else "o" for s in plan.coltor_stages)
+    assert cmodes == "FFFooo"     # ColTor: stage-level while B * pairs >= 256, then operation-level
     ref_rule = G.build_plan(G.DbConfig(16, 16, 16384), p, 1, hw, rule="working_set")
     assert all(s.mode is G.ExecMode.OPERATION_LEVEL for s in ref_rule.expand_stages + ref_rule.coltor_stages)
 
