@@ -88,7 +88,7 @@ struct gpir_db {
   uint32_t d0 = 0, d1 = 0;
   DevBuf data;  // (d1, d0, k, n) brv
   DevBuf d8;    // tensor-core byte planes D8[p][c][ntile][plane][g][NT][16], packed on first use
-  int d8_nt = 0;
+  int d8_nt = 0, d8_kc = 0;
 };
 
 struct gpir_ctx {
@@ -485,27 +485,37 @@ struct Engine {
       const int RA = M <= 128 ? M : 128;  // rows per A tile
       const int mtiles = (M + RA - 1) / RA;
       const bool m64 = RA <= 64;
-      const int NT = (m64 && db->d1 >= 64) ? 64 : 32;  // two TMEM accumulator buffers either way
+      static const int nt_env = getenv("GPIR_TC_NT") ? atoi(getenv("GPIR_TC_NT")) : 0;
+      static const int ord_env = getenv("GPIR_TC_ORDER") ? atoi(getenv("GPIR_TC_ORDER")) : -1;
+      // N = 64 columns per tile when M = 64 (both TMEM accumulator buffers
+      // still fit, lane-interleaved); M = 128 tiles use N = 32 with two
+      // 7 x 32-column buffers so the epilogue overlaps the next item's MMAs
+      const int NT = (nt_env == 32 || nt_env == 64) ? nt_env : (m64 && db->d1 >= 64 ? 64 : 32);
       static const int pst_env = getenv("GPIR_TC_PST") ? atoi(getenv("GPIR_TC_PST")) : 0;
       // p per staged epilogue flush: the staging buffer competes with the TMA
       // pipeline for shared memory, so the M64 x N64 tile stages 4 p (4 stages
       // in flight) rather than 8 (2 stages)
-      const int PST = (pst_env == 2 || pst_env == 4 || pst_env == 8) ? pst_env : (m64 ? (NT == 64 ? 4 : 8) : 4);
-      const int nchunks = ((int)db->d0 + TC_KC - 1) / TC_KC;
+      const int PST = (!m64 && NT == 64)                           ? 2  // only instantiation
+                      : (pst_env == 2 || pst_env == 4 || pst_env == 8) ? pst_env
+                      : m64                                      ? (NT == 64 ? 4 : 8)
+                                                                 : (NT == 64 ? 2 : 8);
+      const int KC = m64 ? 64 : 32;
+      const int nchunks = ((int)db->d0 + KC - 1) / KC;
       const int ntiles = ((int)db->d1 + NT - 1) / NT;
-      if (db->d8_nt != NT) {
-        if ((rc = db->d8.ensure((size_t)KN * nchunks * ntiles * 4 * NT * TC_KC))) return rc;
+      if (db->d8_nt != NT || db->d8_kc != KC) {
+        if ((rc = db->d8.ensure((size_t)KN * nchunks * ntiles * 4 * NT * KC))) return rc;
         CK(cudaMemsetAsync(db->d8.p, 0, db->d8.bytes, s));
         PackSrc ps{db->data.as<u32>(), (size_t)db->d0 * KN, 0, 1, (size_t)KN};
-        dim3 g(KN / PK_P, (ntiles * NT + PK_R - 1) / PK_R, nchunks * (TC_KC / PK_K));
-        k_pack_planes<<<g, 256, 0, s>>>(ps, (int)db->d1, (int)db->d0, NT, ntiles, nchunks, db->d8.as<uint8_t>());
+        dim3 g(KN / PK_P, (ntiles * NT + PK_R - 1) / PK_R, nchunks * (KC / PK_K));
+        k_pack_planes<<<g, 256, 0, s>>>(ps, (int)db->d1, (int)db->d0, NT, ntiles, nchunks, KC, db->d8.as<uint8_t>());
         CKL();
         db->d8_nt = NT;
+        db->d8_kc = KC;
       }
-      if ((rc = c->ws_a8.ensure((size_t)KN * nchunks * mtiles * 4 * RA * TC_KC))) return rc;
+      if ((rc = c->ws_a8.ensure((size_t)KN * nchunks * mtiles * 4 * RA * KC))) return rc;
       PackSrc pa{leaves, a_b_words, (size_t)KN, 2, 2 * (size_t)KN};
-      dim3 g(KN / PK_P, (mtiles * RA + PK_R - 1) / PK_R, nchunks * (TC_KC / PK_K));
-      k_pack_planes<<<g, 256, 0, s>>>(pa, M, (int)db->d0, RA, mtiles, nchunks, c->ws_a8.as<uint8_t>());
+      dim3 g(KN / PK_P, (mtiles * RA + PK_R - 1) / PK_R, nchunks * (KC / PK_K));
+      k_pack_planes<<<g, 256, 0, s>>>(pa, M, (int)db->d0, RA, mtiles, nchunks, KC, c->ws_a8.as<uint8_t>());
       CKL();
       if (ev_mid) CK(cudaEventRecord(ev_mid, s));
       TcArgs ta;
@@ -521,7 +531,8 @@ struct Engine {
       ta.KN = KN;
       ta.logn = LOGN;
       ta.items = KN * ntiles * mtiles;
-      const uint32_t stage_bytes = ((4u * RA * TC_KC + 4u * NT * TC_KC) + 127u) & ~127u;
+      ta.nt_outer = ord_env >= 0 ? ord_env : 0;
+      const uint32_t stage_bytes = ((4u * RA * KC + 4u * NT * KC) + 127u) & ~127u;
       const size_t outbuf = (size_t)PST * RA * (NT + 1) * 4;
       const size_t fixed = 4096 + outbuf + 2 * TC_MAX_STAGES * 8 + 4 * 8 + 16;
       ta.stages = std::max(2, std::min<int>(TC_MAX_STAGES, (int)((226u * 1024u - fixed) / stage_bytes)));
@@ -535,11 +546,16 @@ struct Engine {
         CK(cudaMemsetAsync(profbuf.p, 0, profbuf.bytes, s));
         ta.prof = profbuf.as<unsigned long long>();
       }
-      auto kern = NT == 64 ? (PST == 8 ? k_rowsel_tc<64, true, 8> : PST == 4 ? k_rowsel_tc<64, true, 4>
-                                                                             : k_rowsel_tc<64, true, 2>)
-                  : m64 ? (PST == 8 ? k_rowsel_tc<32, true, 8> : PST == 4 ? k_rowsel_tc<32, true, 4>
-                                                                          : k_rowsel_tc<32, true, 2>)
-                        : (PST == 2 ? k_rowsel_tc<32, false, 2> : k_rowsel_tc<32, false, 4>);
+      auto kern = m64 ? (NT == 64 ? (PST == 8   ? k_rowsel_tc<64, true, 8, 64>
+                                     : PST == 4 ? k_rowsel_tc<64, true, 4, 64>
+                                                : k_rowsel_tc<64, true, 2, 64>)
+                                  : (PST == 8   ? k_rowsel_tc<32, true, 8, 64>
+                                     : PST == 4 ? k_rowsel_tc<32, true, 4, 64>
+                                                : k_rowsel_tc<32, true, 2, 64>))
+                      : (NT == 64 ? k_rowsel_tc<64, false, 2, 32>
+                                  : (PST == 2   ? k_rowsel_tc<32, false, 2, 32>
+                                     : PST == 4 ? k_rowsel_tc<32, false, 4, 32>
+                                                : k_rowsel_tc<32, false, 8, 32>));
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<grid, TC_THREADS, smem, s>>>(ta, c->tb);
       CKL();

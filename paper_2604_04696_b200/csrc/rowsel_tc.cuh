@@ -26,8 +26,10 @@
 
 namespace gpir {
 
-constexpr int TC_KC = 64;        // K bytes per pipeline stage
-constexpr int TC_MAX_STAGES = 8;
+// K bytes per pipeline stage (KC, a kernel template parameter): 64 for the
+// M = 64 tiles, 32 (one MMA K step) for M = 128 tiles, whose larger stages
+// would otherwise leave room for too few of them next to the epilogue staging
+constexpr int TC_MAX_STAGES = 12;
 constexpr int TC_EPI_WARPS = 8;  // two warps per TMEM lane quadrant, each owning half the columns
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 
@@ -106,12 +108,12 @@ __device__ __forceinline__ size_t pack_src_off(const PackSrc& s, int r) {
 // each thread turns 2 rows x 16 k of one p into 4 planes x 32 contiguous bytes.
 constexpr int PK_P = 128, PK_R = 4, PK_K = 16;
 __global__ void __launch_bounds__(256)
-    k_pack_planes(PackSrc src, int R, int Kd, int RT, int ntiles, int nchunks, uint8_t* __restrict__ dst) {
+    k_pack_planes(PackSrc src, int R, int Kd, int RT, int ntiles, int nchunks, int kc, uint8_t* __restrict__ dst) {
   __shared__ __align__(16) u32 tile[PK_R][PK_K][PK_P];
   const int p0 = blockIdx.x * PK_P;
   const int r0 = blockIdx.y * PK_R;
   const int kg = blockIdx.z;  // global 16-byte K group
-  const int c = kg / (TC_KC / PK_K), g = kg % (TC_KC / PK_K);
+  const int c = kg / (kc / PK_K), g = kg % (kc / PK_K);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint4 vals[8];
 #pragma unroll
@@ -149,10 +151,10 @@ __global__ void __launch_bounds__(256)
                                    __byte_perm(v[2], v[3], pl | ((pl + 4) << 4)), 0x5410);
     }
   const int nt = r / RT, rin = r % RT;  // rows r, r+1 share the tile (RT even)
-  const size_t blk = (((size_t)(p0 + pp) * nchunks + c) * ntiles + nt) * (size_t)(4 * RT * TC_KC);
+  const size_t blk = (((size_t)(p0 + pp) * nchunks + c) * ntiles + nt) * (size_t)(4 * RT * kc);
 #pragma unroll
   for (int pl = 0; pl < 4; ++pl) {
-    uint4* d = reinterpret_cast<uint4*>(dst + blk + (size_t)pl * RT * TC_KC + ((size_t)g * RT + rin) * 16);
+    uint4* d = reinterpret_cast<uint4*>(dst + blk + (size_t)pl * RT * kc + ((size_t)g * RT + rin) * 16);
     d[0] = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
     d[1] = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
   }
@@ -169,6 +171,7 @@ struct TcArgs {
   int d1, ntiles, nchunks, KN, logn;
   int items;          // KN * ntiles
   int stages;         // pipeline depth (<= TC_MAX_STAGES)
+  int nt_outer;       // schedule order inside a block of PST p: (nt, mt) or (mt, nt)
   unsigned long long* prof;  // optional per-CTA cycle counters [grid][8] (GPIR_TC_PROF)
 };
 
@@ -185,7 +188,15 @@ struct TcSched {
   __device__ __forceinline__ void next(const TcArgs& a) {
     if (++j == PST) {
       j = 0;
-      if (++nt == a.ntiles) {
+      if (a.nt_outer) {  // row tiles inner: one DB tile stays hot while every row tile streams past it
+        if (++mt == a.mtiles) {
+          mt = 0;
+          if (++nt == a.ntiles) {
+            nt = 0;
+            blk += gridDim.x;
+          }
+        }
+      } else if (++nt == a.ntiles) {
         nt = 0;
         if (++mt == a.mtiles) {
           mt = 0;
@@ -196,7 +207,7 @@ struct TcSched {
   }
 };
 
-template <int TC_NT, bool M64, int TC_PST>
+template <int TC_NT, bool M64, int TC_PST, int TC_KC>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb) {
   using Sched = TcSched<TC_PST>;
   constexpr int TC_ACC_COLS = 7 * TC_NT;
