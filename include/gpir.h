@@ -9,6 +9,10 @@
  *                                               gpir_answer_batch_dev (device buffers)
  *   cluster._answer_shard src/cluster.py:252-265 -> gpir_shard_answer
  *   col_tournament_batch src/protocol.py:542-573 -> gpir_coltor_dev
+ *   wire.deserialize_query / serialize_response / deserialize_evkset
+ *                    src/wire.py:263-318   -> gpir_wire_* (batch collector codec)
+ *   wire.save_database / load_database
+ *                    src/wire.py:365-410   -> gpir_db_save / gpir_db_load
  * Operator-level parity entry points (host buffers, reference natural order):
  *   ntt_raw / intt_raw      src/ring.py:408-453     -> gpir_op_ntt
  *   DigitExtractor          src/he.py:323-367       -> gpir_op_digits
@@ -48,7 +52,8 @@ enum gpir_status {
   GPIR_INVALID_STATE = -2,    /* latpir.errors.InvalidState    */
   GPIR_INVALID_CONFIG = -3,   /* latpir.errors.InvalidConfig   */
   GPIR_CUDA_ERROR = -4,
-  GPIR_UNSUPPORTED = -5
+  GPIR_UNSUPPORTED = -5,
+  GPIR_PARSE_ERROR = -6       /* latpir.errors.ParseError; offset: gpir_last_error_offset() */
 };
 
 typedef struct gpir_stats {
@@ -64,6 +69,8 @@ typedef struct gpir_stats {
 } gpir_stats;
 
 const char* gpir_last_error(void);
+/* byte offset of the last GPIR_PARSE_ERROR (ParseError.offset) */
+int64_t gpir_last_error_offset(void);
 const char* gpir_version(void);
 
 /* Context: ring degree n (power of two), k primes q[i] with 2n-th roots psi[i]
@@ -86,6 +93,14 @@ int gpir_supported(uint32_t n, uint32_t k, uint32_t ell);
 gpir_db* gpir_db_encode(gpir_ctx* ctx, const uint8_t* records, uint32_t d0, uint32_t d1, uint32_t record_bytes,
                         uint32_t plain_bits);
 gpir_db* gpir_db_upload(gpir_ctx* ctx, const uint32_t* pmajor, uint32_t d0, uint32_t d1);
+/* GPDB container (wire.save_database / load_database, src/wire.py:365-410):
+ * load validates magic, version and the primes against the context (and the
+ * plain modulus when expect_plain_bits != 0), streams the payload to the GPU
+ * and transposes a TRANSPOSED image there; errors are GPIR_PARSE_ERROR with the
+ * reference's message and offset.  save writes a P-major image. */
+gpir_db* gpir_db_load(gpir_ctx* ctx, const char* path, uint32_t expect_plain_bits, uint32_t* d0, uint32_t* d1,
+                      uint32_t* record_bytes, uint32_t* plain_bits);
+int gpir_db_save(gpir_ctx* ctx, const gpir_db* db, const char* path, uint32_t record_bytes, uint32_t plain_bits);
 /* Download the encoded DB back as the reference's P-major natural tensor. */
 int gpir_db_download(gpir_ctx* ctx, const gpir_db* db, uint32_t* pmajor_out);
 void gpir_db_destroy(gpir_ctx* ctx, gpir_db* db);
@@ -144,6 +159,23 @@ int gpir_sharded_expand(gpir_ctx* ctx, uint32_t d0, uint32_t d1, const uint32_t*
 int gpir_sharded_rowsel(gpir_ctx* ctx, const gpir_db* db, const uint32_t* d_rows, uint32_t B, uint32_t* d_partial,
                         void* stream);
 int gpir_sharded_coltor(gpir_ctx* ctx, uint32_t* d_sums, uint32_t B_own, uint32_t* d_out, void* stream);
+
+/* ---- wire codec (src/wire.py; host only, usable without a GPU) ----
+ * A batch collector decodes the framed query messages of a batch straight into
+ * one contiguous host buffer queries[count][2][k][n] (pass it pinned to
+ * gpir_answer_batch) and encodes responses back into framed bytes, with the
+ * reference's validation and ParseError offsets.  bad_index (may be NULL)
+ * receives the index of the message being decoded when an error occurs. */
+int gpir_wire_parse_header(const uint8_t* buf, size_t len, uint32_t* kind, uint64_t* payload_len);
+int gpir_wire_decode_queries(const uint8_t* const* msgs, const size_t* lens, uint32_t count, uint32_t n, uint32_t k,
+                             uint32_t* queries, uint64_t* client_ids, uint32_t* seqs, uint32_t* bad_index);
+size_t gpir_wire_response_bytes(uint32_t n, uint32_t k);
+int gpir_wire_encode_responses(const uint32_t* responses, const uint64_t* client_ids, const uint32_t* seqs,
+                               uint32_t count, uint32_t n, uint32_t k, uint8_t* out, size_t out_cap);
+/* KIND_EVKSET (serialize_evkset) -> gpir_keys_put layout: evks[stages][ell][2][k][n]
+ * by stage (k_aut = n/2^t + 1), sk_rgsw[2 ell][2][k][n] (may be NULL). */
+int gpir_wire_decode_evkset(const uint8_t* msg, size_t len, uint32_t n, uint32_t k, uint32_t z_bits, uint32_t ell,
+                            uint32_t stages, uint32_t* evks, uint32_t* sk_rgsw, uint64_t* client_id, int* has_rgsw);
 
 /* ---- operator-level parity entry points (host buffers, natural order) ---- */
 int gpir_op_ntt(gpir_ctx* ctx, const uint32_t* in, uint32_t* out, uint32_t polys, int inverse);

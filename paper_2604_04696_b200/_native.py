@@ -10,7 +10,7 @@ import ctypes as C
 import os
 import threading
 
-from .errors import InvalidArgument, InvalidConfig, InvalidState, NativeError
+from .errors import InvalidArgument, InvalidConfig, InvalidState, NativeError, ParseError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GPIR_LIB", os.path.join(HERE, "libgpir.so"))
@@ -57,6 +57,17 @@ _SIGS = {
                                       C.c_void_p]),
     "gpir_sharded_rowsel": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
     "gpir_sharded_coltor": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "gpir_last_error_offset": (C.c_int64, []),
+    "gpir_db_load": (C.c_void_p, [C.c_void_p, C.c_char_p, C.c_uint32, _u32p, _u32p, _u32p, _u32p]),
+    "gpir_db_save": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_uint32, C.c_uint32]),
+    "gpir_wire_parse_header": (C.c_int, [C.c_void_p, C.c_size_t, _u32p, C.POINTER(C.c_uint64)]),
+    "gpir_wire_decode_queries": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_uint32, C.c_uint32,
+                                           C.c_uint32, _u32p, C.POINTER(C.c_uint64), _u32p, _u32p]),
+    "gpir_wire_response_bytes": (C.c_size_t, [C.c_uint32, C.c_uint32]),
+    "gpir_wire_encode_responses": (C.c_int, [_u32p, C.POINTER(C.c_uint64), _u32p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                             C.c_void_p, C.c_size_t]),
+    "gpir_wire_decode_evkset": (C.c_int, [C.c_void_p, C.c_size_t, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                          C.c_uint32, _u32p, _u32p, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]),
     "gpir_op_ntt": (C.c_int, [C.c_void_p, _u32p, _u32p, C.c_uint32, C.c_int]),
     "gpir_op_digits": (C.c_int, [C.c_void_p, _u32p, _i32p, C.c_uint32]),
     "gpir_op_expand_stage": (C.c_int, [C.c_void_p, _u32p, C.c_uint32, C.c_uint32, _u32p, C.c_uint32, C.c_int, _u32p]),
@@ -107,6 +118,8 @@ def check(rc: int, what: str = "") -> None:
         raise InvalidState(msg)
     if rc == -3:
         raise InvalidConfig(msg)
+    if rc == -6:  # the reference's message and byte offset, unprefixed
+        raise ParseError(last_error(), int(load().gpir_last_error_offset()))
     raise NativeError(f"{msg} (status {rc})")
 
 

@@ -1072,6 +1072,8 @@ static int db_encode_launch(gpir_ctx* c, const uint8_t* d_recs, int rec_bytes, i
   return 0;
 }
 
+#include "wire_codec.h"
+
 // ---------------------------------------------------------------------------
 // dispatch over compiled (LOGN, K, ELL) combinations
 
@@ -1229,6 +1231,135 @@ gpir_db* gpir_db_upload(gpir_ctx* c, const uint32_t* pmajor, uint32_t d0, uint32
     return nullptr;
   }
   return db;
+}
+
+// ---- GPDB container (save_database / load_database, src/wire.py:365-410) ----
+// Header "<4sHIIIIBBB": magic, version, d0, d1, record_bytes, n, k, plain_bits,
+// layout (0 P-major (d1, d0, p), 1 transposed (p, d1, d0)); k u64 primes; the
+// <u4 payload.  The payload streams through a pinned 64 MiB staging buffer into
+// device memory; a transposed image is transposed on the GPU.
+static const size_t kDbHead = 25;
+
+gpir_db* gpir_db_load(gpir_ctx* c, const char* path, uint32_t expect_plain_bits, uint32_t* d0_out, uint32_t* d1_out,
+                      uint32_t* record_bytes_out, uint32_t* plain_bits_out) {
+  using namespace gpir_wire;
+  g_off = -1;  // set >= 0 only by a parse error
+  if (!c || !path) {
+    g_err = "invalid argument";
+    return nullptr;
+  }
+  FILE* fh = fopen(path, "rb");
+  if (!fh) {
+    g_err = std::string("cannot open ") + path;
+    return nullptr;
+  }
+  struct Closer {
+    FILE* f;
+    ~Closer() { fclose(f); }
+  } closer{fh};
+  uint8_t head[kDbHead];
+  const size_t got = fread(head, 1, kDbHead, fh);
+  auto fail = [&](const std::string& m, int64_t off) -> gpir_db* {
+    parse_fail(m, off);
+    return nullptr;
+  };
+  if (got < kDbHead) return fail("truncated database header", (int64_t)got);
+  if (memcmp(head, kDbMagic, 4) != 0) {
+    char m[64];
+    snprintf(m, sizeof m, "bad database magic b'%c%c%c%c'", head[0], head[1], head[2], head[3]);
+    return fail(m, 0);
+  }
+  const uint16_t ver = rd<uint16_t>(head + 4);
+  if (ver != kVersion) return fail("unsupported database version " + std::to_string(ver), 4);
+  const uint32_t d0 = rd<uint32_t>(head + 6), d1 = rd<uint32_t>(head + 10), rb = rd<uint32_t>(head + 14);
+  const uint32_t n = rd<uint32_t>(head + 18), k = head[22], pb = head[23], layout = head[24];
+  std::vector<uint64_t> qs(k);
+  if (k && fread(qs.data(), 8, k, fh) != k) return fail("truncated database header", (int64_t)kDbHead);
+  bool match = n == c->n && k == c->k && (!expect_plain_bits || expect_plain_bits == pb);
+  for (uint32_t i = 0; match && i < k; ++i) match = qs[i] == c->q[i];
+  if (!match) return fail("database parameters do not match the supplied profile", (int64_t)kDbHead);
+  if (!d0 || !d1 || (d1 & (d1 - 1)) || layout > 1) return fail("bad database geometry", 6);
+  const size_t words = (size_t)d0 * d1 * k * n;
+  std::lock_guard<std::mutex> lk(c->mu);
+  cudaSetDevice(c->device);
+  gpir_db* db = new gpir_db();
+  db->d0 = d0;
+  db->d1 = d1;
+  DevBuf tmp, tr;
+  void* pinned = nullptr;
+  const size_t chunk = (size_t)64 << 20;
+  int rc = tmp.ensure(words * 4);
+  if (!rc) rc = db->data.ensure(words * 4);
+  if (!rc && cudaMallocHost(&pinned, chunk) != cudaSuccess) rc = GPIR_CUDA_ERROR, g_err = "pinned staging";
+  size_t done = 0;
+  while (!rc && done < words * 4) {
+    const size_t want = std::min(chunk, words * 4 - done);
+    const size_t r = fread(pinned, 1, want, fh);
+    if (r < want) {
+      parse_fail("truncated database payload", (int64_t)(kDbHead + done + r));
+      rc = -6;
+      break;
+    }
+    if (cudaMemcpy(tmp.as<uint8_t>() + done, pinned, want, cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = GPIR_CUDA_ERROR, g_err = "db upload failed";
+    done += want;
+  }
+  const u32* pm = tmp.as<u32>();
+  if (!rc && layout == 1) {  // (p, d1, d0) -> (d1, d0, p)
+    rc = tr.ensure(words * 4);
+    if (!rc) {
+      const size_t P = (size_t)k * n, R = (size_t)d1 * d0;
+      dim3 g((unsigned)((R + 31) / 32), (unsigned)((P + 31) / 32));
+      k_transpose32<<<g, dim3(32, 8), 0, c->stream>>>(tmp.as<u32>(), tr.as<u32>(), P, R);
+      if (cudaGetLastError() != cudaSuccess) rc = GPIR_CUDA_ERROR, g_err = "transpose launch";
+      pm = tr.as<u32>();
+    }
+  }
+  if (!rc) rc = bitrev_rows(c, pm, db->data.as<u32>(), words >> c->logn, c->stream);
+  if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = GPIR_CUDA_ERROR, g_err = "db load failed";
+  if (pinned) cudaFreeHost(pinned);
+  tmp.release();
+  tr.release();
+  if (rc) {
+    db->data.release();
+    delete db;
+    return nullptr;
+  }
+  if (d0_out) *d0_out = d0;
+  if (d1_out) *d1_out = d1;
+  if (record_bytes_out) *record_bytes_out = rb;
+  if (plain_bits_out) *plain_bits_out = pb;
+  return db;
+}
+
+int gpir_db_save(gpir_ctx* c, const gpir_db* db, const char* path, uint32_t record_bytes, uint32_t plain_bits) {
+  using namespace gpir_wire;
+  if (!c || !db || !path) FAIL(GPIR_INVALID_ARGUMENT, "invalid argument");
+  const size_t words = (size_t)db->d0 * db->d1 * c->k * c->n;
+  std::vector<uint32_t> host(words);
+  int rc = gpir_db_download(c, db, host.data());
+  if (rc) return rc;
+  FILE* fh = fopen(path, "wb");
+  if (!fh) FAIL(GPIR_INVALID_ARGUMENT, std::string("cannot open ") + path);
+  uint8_t head[kDbHead];
+  memcpy(head, kDbMagic, 4);
+  wr<uint16_t>(head + 4, kVersion);
+  wr<uint32_t>(head + 6, db->d0);
+  wr<uint32_t>(head + 10, db->d1);
+  wr<uint32_t>(head + 14, record_bytes);
+  wr<uint32_t>(head + 18, c->n);
+  head[22] = (uint8_t)c->k;
+  head[23] = (uint8_t)plain_bits;
+  head[24] = 0;  // P-major
+  bool ok = fwrite(head, 1, kDbHead, fh) == kDbHead;
+  for (uint32_t i = 0; ok && i < c->k; ++i) {
+    const uint64_t q = c->q[i];
+    ok = fwrite(&q, 8, 1, fh) == 1;
+  }
+  ok = ok && fwrite(host.data(), 4, words, fh) == words;
+  ok = (fclose(fh) == 0) && ok;
+  if (!ok) FAIL(GPIR_INVALID_ARGUMENT, std::string("write failed: ") + path);
+  return 0;
 }
 
 int gpir_db_download(gpir_ctx* c, const gpir_db* db, uint32_t* out) {

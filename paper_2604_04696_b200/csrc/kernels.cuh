@@ -844,6 +844,17 @@ __global__ void k_mod_rows(u32* __restrict__ x, size_t rows, int logn, int k, Ta
 }
 
 // Bit-reversal permutation of whole limb rows (natural <-> brv; an involution).
+// out[r][p] = in[p][r] for a P x R u32 matrix (32 x 32 tiles through shared memory)
+__global__ void k_transpose32(const u32* __restrict__ in, u32* __restrict__ out, size_t P, size_t R) {
+  __shared__ u32 t[32][33];
+  const size_t r0 = (size_t)blockIdx.x * 32, p0 = (size_t)blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += 8)
+    if (p0 + y < P && r0 + threadIdx.x < R) t[y][threadIdx.x] = in[(p0 + y) * R + r0 + threadIdx.x];
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += 8)
+    if (r0 + y < R && p0 + threadIdx.x < P) out[(r0 + y) * P + p0 + threadIdx.x] = t[threadIdx.x][y];
+}
+
 __global__ void k_bitrev_rows(const u32* __restrict__ in, u32* __restrict__ out, size_t rows, int logn) {
   const size_t n = (size_t)1 << logn;
   const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -353,36 +353,33 @@ def _make_response(query, raw: np.ndarray):
     return resp_t(ct_t(a, b), query.client_id, query.seq)
 
 
-def answer_batch(queries, keys_by_client, db, params, hw: HardwareModel | None = None,
-                 plan: ExecutionPlan | None = None, mode: ExecMode | None = None, engine: str = "auto",
-                 tile=None, pipeline=None, stats: ServeStats | None = None) -> list:
-    """Serve a batch end to end on the GPU (src/protocol.py:635-682).
-
-    Every query uses its own client's keys; responses come back in query order
-    and are independent of batch composition (bit-identical to the reference)."""
-    if not queries:
-        return []
+def answer_raw(qarr: np.ndarray, client_ids, keys_by_client, db, params, hw: HardwareModel | None = None,
+               plan: ExecutionPlan | None = None, mode: ExecMode | None = None, engine: str = "auto",
+               stats: ServeStats | None = None, out: np.ndarray | None = None) -> np.ndarray:
+    """Serve a batch given as one (B, 2, k, n) uint32 array of NTT-domain query
+    ciphertexts (natural slot order) and the per-query client ids; returns the
+    (B, 2, k, n) responses.  This is the path the wire batch collector uses: the
+    decoded bytes go straight in (pinned buffers avoid a staging copy)."""
+    B = int(qarr.shape[0])
     if engine not in _ENGINES:
         raise InvalidArgument(f"unknown row-selection engine {engine!r}")
     config = db.config
     try:
-        keys = [keys_by_client[q.client_id] for q in queries]
+        keys = [keys_by_client[int(c)] for c in client_ids]
     except KeyError as exc:
         raise InvalidState(f"no uploaded keys for client {exc.args[0]}") from None
     ddb = _device_db(db, params)
     ctx = ddb.ctx
-    B = len(queries)
+    if qarr.shape != (B, 2, ctx.k, ctx.n) or qarr.dtype != np.uint32 or not qarr.flags.c_contiguous:
+        raise InvalidArgument(f"queries must be a contiguous uint32 array of shape (B, 2, {ctx.k}, {ctx.n})")
     ell = params.gadget.ell
     total = planner.expansion_leaves(config.d0, config.d1, ell)
     stages = planner.num_expand_stages(total)
     need_rg = config.d1 > 1
     slots = np.array([ctx.key_slot(k, stages, need_rg) for k in keys], dtype=np.int32)
-    qarr = np.empty((B, 2, ctx.k, ctx.n), dtype=np.uint32)
-    for i, q in enumerate(queries):
-        qarr[i, 0] = q.ct.a.limbs
-        qarr[i, 1] = q.ct.b.limbs
     em, cm = _modes(config, params, B, hw, plan, mode)
-    out = np.empty_like(qarr)
+    if out is None:
+        out = np.empty_like(qarr)
     nat.check(ctx.lib.gpir_set_rowsel_engine(ctx.h, _ENGINES[engine]), "rowsel engine")
     st = nat.GpirStats()
     t0 = time.perf_counter()
@@ -400,6 +397,30 @@ def answer_batch(queries, keys_by_client, db, params, hw: HardwareModel | None =
         stats.d2h_seconds += st.ms_d2h / 1e3
         stats.device_seconds += st.ms_total / 1e3
         stats.stages.append(StageTiming("Batch", 0, B, "gpu", 0, wall, 0))
+    return out
+
+
+def answer_batch(queries, keys_by_client, db, params, hw: HardwareModel | None = None,
+                 plan: ExecutionPlan | None = None, mode: ExecMode | None = None, engine: str = "auto",
+                 tile=None, pipeline=None, stats: ServeStats | None = None) -> list:
+    """Serve a batch end to end on the GPU (src/protocol.py:635-682).
+
+    Every query uses its own client's keys; responses come back in query order
+    and are independent of batch composition (bit-identical to the reference)."""
+    if not queries:
+        return []
+    if engine not in _ENGINES:
+        raise InvalidArgument(f"unknown row-selection engine {engine!r}")
+    for q in queries:
+        if q.client_id not in keys_by_client:
+            raise InvalidState(f"no uploaded keys for client {q.client_id}")
+    ctx = _device_db(db, params).ctx
+    qarr = np.empty((len(queries), 2, ctx.k, ctx.n), dtype=np.uint32)
+    for i, q in enumerate(queries):
+        qarr[i, 0] = q.ct.a.limbs
+        qarr[i, 1] = q.ct.b.limbs
+    out = answer_raw(qarr, [q.client_id for q in queries], keys_by_client, db, params, hw=hw, plan=plan,
+                     mode=mode, engine=engine, stats=stats)
     return [_make_response(q, out[i]) for i, q in enumerate(queries)]
 
 
