@@ -321,36 +321,51 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
-def run_rowshard(args, rank, world, local_rank):
-    """North-star multi-GPU mode: DB rows sharded over the ranks, queries owned
-    round-robin in blocks, NCCL all-to-all + reduce-scatter(sum) combine
-    (paper_2604_04696_b200/cluster.py).  Strong scaling: the config's DB and
-    batch are fixed and split over the ranks."""
+def run_sharded(args, rank, world, local_rank):
+    """Multi-GPU sharded serving (paper_2604_04696_b200/cluster.py), strong
+    scaling: the config's DB and batch are fixed and split over the ranks.
+    rowshard: DB rows + query owners, NCCL all-to-all + reduce-scatter(sum)
+    (the north star's modular-add combine).  colshard: DB columns + query owners,
+    NCCL all-gather of the row cts + all-to-all of one partial per query (the
+    reference's SHARD_ALL_GATHER)."""
     import torch
     import torch.distributed as dist
 
     import paper_2604_04696_b200 as G
-    from paper_2604_04696_b200.cluster import CudaRowShard, TorchComm, answer_row_sharded
+    from paper_2604_04696_b200.cluster import (CudaColShard, CudaRowShard, TorchComm, answer_col_sharded,
+                                               answer_row_sharded)
 
     torch.cuda.set_device(local_rank)
     d0, d1, B, rb, pb, desc = CONFIGS[args.config]
-    if B % world or d0 % world:
-        raise SystemExit(f"batch {B} / d0 {d0} do not split over {world} ranks")
+    col = args.strategy == "colshard"
+    if B % world or (d1 if col else d0) % world:
+        raise SystemExit(f"batch {B} / {'d1' if col else 'd0'} do not split over {world} ranks")
     params = G.HeParams(G.default_basis(4096), pb)
-    d0l, b_own = d0 // world, B // world
+    b_own = B // world
     rng = np.random.default_rng(500 + rank)
-    rows = rng.integers(0, 256, size=(d0l * d1, rb), dtype=np.uint8)
-    be = CudaRowShard(params, rows, d0, d1, rb, world, local_rank)
-    del rows
+    if col:
+        recs = rng.integers(0, 256, size=(d0 * (d1 // world), rb), dtype=np.uint8)
+        be = CudaColShard(params, recs, d0, d1, rb, world, local_rank)
+    else:
+        recs = rng.integers(0, 256, size=((d0 // world) * d1, rb), dtype=np.uint8)
+        be = CudaRowShard(params, recs, d0, d1, rb, world, local_rank)
+    del recs
     stages = G.planner.num_expand_stages(G.planner.expansion_leaves(d0, d1, params.gadget.ell))
     evks, rgsw, queries = synthetic_material(G, params, b_own, stages, rng)
     for b in range(b_own):
         be.put_keys(b, evks[b], rgsw[b])
     slots = np.arange(b_own, dtype=np.int32)
     q = torch.from_numpy(queries.view(np.int32)).cuda()
-    comm = TorchComm() if world > 1 else type("C1", (), {"size": 1, "all_to_all": staticmethod(lambda x: x),
-                                                         "reduce_scatter_sum": staticmethod(lambda x: x[0])})()
-    step = lambda: answer_row_sharded(be, comm, q, slots, d0, d1)
+
+    class _One:  # world 1: the collectives are identities
+        size = 1
+        all_to_all = staticmethod(lambda x: x)
+        reduce_scatter_sum = staticmethod(lambda x: x[0])
+        all_gather = staticmethod(lambda x: x.unsqueeze(0))
+
+    comm = TorchComm() if world > 1 else _One()
+    answer = answer_col_sharded if col else answer_row_sharded
+    step = lambda: answer(be, comm, q, slots, d0, d1)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -370,13 +385,15 @@ def run_rowshard(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     if rank == 0:
+        par = (f"colshard{world} (DB columns + query owners; NCCL all-gather + all-to-all)" if col else
+               f"rowshard{world} (DB rows + query owners; NCCL all-to-all + reduce-scatter)")
         line = {
             "metric": "PIR queries/sec (batched)", "value": B / (ms / 1e3), "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32 (mod-q, 64-bit lazy products)",
             "data": "synthetic (random records, uniform-random key/query material)",
             "config": {"workload": desc, "d0": d0, "d1": d1, "global_batch": B, "record_bytes": rb, "plain_bits": pb,
-                       "parallelism": f"rowshard{world} (DB rows + query owners; NCCL all-to-all + reduce-scatter)"},
+                       "parallelism": par},
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -391,8 +408,9 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--modes", default="", help='"fused", "op", or an explicit plan "EQ/CT" (o/F/S/H per stage)')
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--strategy", default="replica", choices=["replica", "rowshard"],
-                    help="multi-GPU mode: replica (DB copy + own batch per GPU) or rowshard (north-star DB row shards)")
+    ap.add_argument("--strategy", default="replica", choices=["replica", "rowshard", "colshard"],
+                    help="multi-GPU mode: replica (DB copy + own batch per GPU), rowshard (north-star DB row "
+                         "shards, modular-add combine) or colshard (DB column shards, all-gather)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -409,8 +427,8 @@ def main():
             dist.init_process_group("gloo")
     if args.impl == "reference":
         run_reference(args, rank, world)
-    elif args.strategy == "rowshard":
-        run_rowshard(args, rank, world, local_rank)
+    elif args.strategy in ("rowshard", "colshard"):
+        run_sharded(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
     if world > 1:

@@ -159,6 +159,14 @@ int gpir_sharded_expand(gpir_ctx* ctx, uint32_t d0, uint32_t d1, const uint32_t*
 int gpir_sharded_rowsel(gpir_ctx* ctx, const gpir_db* db, const uint32_t* d_rows, uint32_t B, uint32_t* d_partial,
                         void* stream);
 int gpir_sharded_coltor(gpir_ctx* ctx, uint32_t* d_sums, uint32_t B_own, uint32_t* d_out, void* stream);
+/* Column-sharded mode (src/cluster.py SHARD_ALL_GATHER over NCCL): after
+ * gpir_sharded_expand, export the own queries' RGSW rows of column bits
+ * [bit_lo, bit_hi) in natural order as d_rgsw[B_own][bit_hi-bit_lo][2 ell][2][k][n]
+ * (the layout gpir_coltor_dev takes). */
+int gpir_sharded_rgsw(gpir_ctx* ctx, uint32_t bit_lo, uint32_t bit_hi, uint32_t* d_rgsw, void* stream);
+/* natural <-> internal bit-reversed slot order of `polys` ciphertext halves
+ * ([polys][k][n] words; an involution), device buffers. */
+int gpir_layout_convert(gpir_ctx* ctx, const uint32_t* d_in, uint32_t* d_out, uint64_t polys, void* stream);
 
 /* ---- wire codec (src/wire.py; host only, usable without a GPU) ----
  * A batch collector decodes the framed query messages of a batch straight into

@@ -57,6 +57,8 @@ _SIGS = {
                                       C.c_void_p]),
     "gpir_sharded_rowsel": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
     "gpir_sharded_coltor": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "gpir_sharded_rgsw": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "gpir_layout_convert": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "gpir_last_error_offset": (C.c_int64, []),
     "gpir_db_load": (C.c_void_p, [C.c_void_p, C.c_char_p, C.c_uint32, _u32p, _u32p, _u32p, _u32p]),
     "gpir_db_save": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_uint32, C.c_uint32]),

@@ -1,4 +1,5 @@
-"""Multi-GPU serving: the database row-sharded across ranks (one process per GPU).
+"""Multi-GPU serving: the database row-sharded (north star) or column-sharded
+(the reference's SHARD_ALL_GATHER) across ranks, one process per GPU.
 
 North-star mode: rank r of n owns DB rows
 [r d0/n, (r+1) d0/n) x all d1 columns and the queries [r B/n, (r+1) B/n).
@@ -61,6 +62,46 @@ def answer_row_sharded(backend, comm, queries_own, slots_own, d0: int, d1: int):
     return backend.coltor(sums.reshape(b_own, d1, ct))
 
 
+def answer_col_sharded(backend, comm, queries_own, slots_own, d0: int, d1: int):
+    """Column-sharded serving (the reference's SHARD_ALL_GATHER strategy,
+    src/cluster.py:350-440, with NCCL collectives instead of worker threads).
+
+    Rank r of n owns DB columns [r d1/n, (r+1) d1/n) x all d0 rows and the
+    queries [r B/n, (r+1) B/n).
+      1. every rank expands its OWN queries over the full tree and assembles
+         their RGSWs;
+      2. all-gather of the row ciphertexts (B x d0 cts; the reference's
+         after_expand volume) and of the low-bit RGSW rows (its sidecar);
+      3. local RowSel over the rank's columns for all B queries and the low
+         log2(d1/n) ColTor stages -> one partial ciphertext per query;
+      4. all-to-all of the partials to the query owners (the reference's
+         after_coltor volume, B x n cts);
+      5. the owner finishes the top log2(n) ColTor stages.
+    The exchange volume does not depend on d1, so it scales with the DB.
+
+    backend: .expand(queries_own, slots_own) -> (rows (B_own, d0, CT), rgsw (B_own, bits, 2 ELL, CT))
+             .rowsel_coltor(rows_all (B, d0, CT), rgsw_low (B, low, 2 ELL, CT)) -> (B, CT)
+             .coltor(parts (B_own, n, CT), rgsw_high (B_own, bits - low, 2 ELL, CT)) -> (B_own, CT)
+    comm:    .size, .all_gather(x) -> (n, *x.shape), .all_to_all(send (n, ...)) -> (n, ...)
+    """
+    n = comm.size
+    if d1 % n or (n & (n - 1)):
+        raise InvalidArgument(f"d1={d1} does not split into {n} power-of-two column shards")
+    low = (d1 // n).bit_length() - 1
+    rows, rgsw = backend.expand(queries_own, slots_own)
+    b_own = rows.shape[0]
+    rows_all = comm.all_gather(rows)                       # (n, B_own, d0, CT), rank order = query order
+    if low:
+        rg_low = comm.all_gather(rgsw[:, :low].contiguous())  # (n, B_own, low, 2 ELL, CT)
+    else:
+        rg_low = rgsw[:, :0].unsqueeze(0).expand((n,) + tuple(rgsw[:, :0].shape)).contiguous()
+    part = backend.rowsel_coltor(rows_all.reshape((n * b_own,) + tuple(rows.shape[1:])),
+                                 rg_low.reshape((n * b_own,) + tuple(rg_low.shape[2:])))
+    recv = comm.all_to_all(part.reshape((n, b_own) + tuple(part.shape[1:])))  # recv[s] = shard s's partials
+    parts = recv.transpose(0, 1).contiguous()              # (B_own, n, CT): ct index = column shard
+    return backend.coltor(parts, rgsw[:, low:].contiguous())
+
+
 class TorchComm:
     """torch.distributed transport (NCCL on GPUs, gloo on CPU)."""
 
@@ -78,6 +119,14 @@ class TorchComm:
         recv = torch.empty_like(send)
         self.dist.all_to_all_single(recv, send, group=self.group)
         return recv
+
+    def all_gather(self, x):
+        import torch
+
+        x = x.contiguous()
+        out = torch.empty((self.size * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        self.dist.all_gather_into_tensor(out, x, group=self.group)  # concatenated along dim 0
+        return out.view((self.size,) + tuple(x.shape))
 
     def reduce_scatter_sum(self, x):
         import torch
@@ -157,4 +206,80 @@ class CudaRowShard:
         out = t.empty((b_own, self.ct), dtype=t.int32, device=f"cuda:{self.device}")
         nat.check(self.ctx.lib.gpir_sharded_coltor(self.ctx.h, C.c_void_p(sums.data_ptr()), b_own,
                                                    C.c_void_p(out.data_ptr()), self._sp()), "sharded coltor")
+        return out
+
+
+class CudaColShard:
+    """Product backend of `answer_col_sharded`: libgpir entry points on this
+    rank's GPU.  `db_cols` holds this rank's column shard of the record grid as
+    a (d0 * d1/n, record_bytes) uint8 array in row-major (i, j_local) order."""
+
+    def __init__(self, params, db_cols: np.ndarray, d0: int, d1: int, record_bytes: int, n: int, device: int):
+        import torch
+
+        from .values import DbConfig
+
+        self.torch = torch
+        self.params = params
+        self.d0, self.d1, self.n = d0, d1, n
+        self.device = device
+        self.ctx = Context(params, device)
+        cfg = DbConfig(d0, d1 // n, record_bytes)
+        recs = np.ascontiguousarray(db_cols, dtype=np.uint8)
+        if recs.shape != (cfg.records, record_bytes):
+            raise InvalidArgument(f"column shard shape {recs.shape} != {(cfg.records, record_bytes)}")
+        h = self.ctx.lib.gpir_db_encode(self.ctx.h, nat.ptr(recs, C.c_uint8), cfg.d0, cfg.d1, record_bytes,
+                                        params.plain_bits)
+        if not h:
+            raise nat.NativeError(f"gpir_db_encode failed: {nat.last_error()}")
+        self.db = EncodedDatabase(cfg, params, self.ctx, h)
+        b = params.basis
+        self.k, self.nn, self.ell = b.k, b.n, params.gadget.ell
+        self.ct = 2 * b.k * b.n
+        self.bits = d1.bit_length() - 1
+        self.stream = torch.cuda.current_stream(device)
+
+    def _sp(self):
+        return C.c_void_p(self.stream.cuda_stream)
+
+    def _new(self, *shape):
+        return self.torch.empty(shape, dtype=self.torch.int32, device=f"cuda:{self.device}")
+
+    def put_keys(self, slot: int, evks: np.ndarray, sk_rgsw: np.ndarray | None):
+        ev = np.ascontiguousarray(evks, dtype=np.uint32)
+        rg = None if sk_rgsw is None else np.ascontiguousarray(sk_rgsw, dtype=np.uint32)
+        nat.check(self.ctx.lib.gpir_keys_put(self.ctx.h, slot, nat.ptr(ev), ev.shape[0], nat.ptr(rg)), "keys")
+
+    def expand(self, queries_own, slots_own):
+        lib, h = self.ctx.lib, self.ctx.h
+        b_own = queries_own.shape[0]
+        rows = self._new(b_own, self.d0, self.ct)
+        nat.check(lib.gpir_sharded_expand(h, self.d0, self.d1, C.c_void_p(queries_own.data_ptr()),
+                                          nat.ptr(slots_own, C.c_int32), b_own, C.c_void_p(rows.data_ptr()),
+                                          self._sp()), "sharded expand")
+        rg = self._new(b_own, self.bits, 2 * self.ell, self.ct)
+        if self.bits:
+            nat.check(lib.gpir_sharded_rgsw(h, 0, self.bits, C.c_void_p(rg.data_ptr()), self._sp()), "sharded rgsw")
+        return rows, rg
+
+    def rowsel_coltor(self, rows_all, rgsw_low):
+        lib, h = self.ctx.lib, self.ctx.h
+        B, d1l = rows_all.shape[0], self.d1 // self.n
+        sel = self._new(B, d1l, self.ct)
+        nat.check(lib.gpir_sharded_rowsel(h, self.db.handle, C.c_void_p(rows_all.data_ptr()), B,
+                                          C.c_void_p(sel.data_ptr()), self._sp()), "sharded rowsel")
+        nat_sel = self._new(B, d1l, self.ct)  # internal slot order -> natural for the tournament
+        nat.check(lib.gpir_layout_convert(h, C.c_void_p(sel.data_ptr()), C.c_void_p(nat_sel.data_ptr()),
+                                          B * d1l * 2, self._sp()), "layout")
+        out = self._new(B, self.ct)
+        nat.check(lib.gpir_coltor_dev(h, C.c_void_p(nat_sel.data_ptr()), B, d1l, C.c_void_p(rgsw_low.data_ptr()),
+                                      C.c_void_p(out.data_ptr()), self._sp()), "local coltor")
+        return out
+
+    def coltor(self, parts, rgsw_high):
+        b_own = parts.shape[0]
+        out = self._new(b_own, self.ct)
+        nat.check(self.ctx.lib.gpir_coltor_dev(self.ctx.h, C.c_void_p(parts.data_ptr()), b_own, self.n,
+                                               C.c_void_p(rgsw_high.data_ptr()), C.c_void_p(out.data_ptr()),
+                                               self._sp()), "owner coltor")
         return out

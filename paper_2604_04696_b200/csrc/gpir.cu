@@ -842,6 +842,27 @@ struct Engine {
 
   // ColTor for the session's own queries from combined RowSel sums (int32,
   // brv, sum of shard partials < n q): reduce mod q, run all log2(d1) stages.
+  // RGSW rows of column bits [lo, hi) for the session's own queries (after
+  // sh_expand), natural order, as (B, hi - lo, 2 ELL) ciphertexts: a-digit rows
+  // from the RGSW assembly, b-digit rows = the column leaves (src/protocol.py:383-409).
+  static int sh_rgsw(gpir_ctx* c, uint32_t lo, uint32_t hi, u32* d_out, cudaStream_t s) {
+    if (!c->sh_leaves) FAIL(GPIR_INVALID_STATE, "gpir_sharded_expand must precede gpir_sharded_rgsw");
+    const uint32_t bits = ilog2(c->sh_d1), B = c->sh_B, total = c->sh_total, d0 = c->sh_d0;
+    if (lo > hi || hi > bits) FAIL(GPIR_INVALID_ARGUMENT, "bit range outside the session's tournament");
+    const uint32_t nb = hi - lo;
+    int rc;
+    for (uint32_t b = 0; b < B; ++b)
+      for (uint32_t h = 0; h < nb; ++h) {
+        const uint32_t j = lo + h;
+        u32* dst = d_out + (((size_t)b * nb + h) * 2 * ELL) * CT;
+        const u32* a_rows = c->ws_arows.as<u32>() + ((size_t)b * bits + j) * ELL * CT;
+        const u32* b_rows = c->sh_leaves + ((size_t)b * total + d0 + j * ELL) * CT;
+        if ((rc = bitrev_rows(c, a_rows, dst, (size_t)ELL * 2 * K, s))) return rc;
+        if ((rc = bitrev_rows(c, b_rows, dst + (size_t)ELL * CT, (size_t)ELL * 2 * K, s))) return rc;
+      }
+    return 0;
+  }
+
   static int sh_coltor(gpir_ctx* c, u32* d_sums, int B, u32* d_out, cudaStream_t s) {
     if (!c->sh_leaves || (uint32_t)B != c->sh_B) FAIL(GPIR_INVALID_STATE, "gpir_sharded_expand must precede gpir_sharded_coltor");
     const uint32_t d1 = c->sh_d1, bits = ilog2(d1), total = c->sh_total, d0 = c->sh_d0;
@@ -1590,6 +1611,37 @@ int gpir_sharded_rowsel(gpir_ctx* c, const gpir_db* db, const uint32_t* d_rows, 
     case 60206: rc = Engine<6, 2, 6>::rowsel(c, d_rows, (size_t)db->d0 * c->ct_words(), (int)B, mdb, d_partial, s, &launches); break;
     default: FAIL(GPIR_UNSUPPORTED, "unsupported combination");
   }
+  if (rc) return rc;
+  if (!stream) CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+#define DISPATCH_CASE_SHR(L, K_, E) \
+  case L * 10000 + K_ * 100 + E:    \
+    rc = Engine<L, K_, E>::sh_rgsw(c, bit_lo, bit_hi, d_rgsw, s); break;
+
+int gpir_sharded_rgsw(gpir_ctx* c, uint32_t bit_lo, uint32_t bit_hi, uint32_t* d_rgsw, void* stream) {
+  if (!c || !d_rgsw) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  int rc;
+  switch (c->logn * 10000 + c->k * 100 + c->ell) {
+    GPIR_COMBOS(DISPATCH_CASE_SHR)
+    default:
+      FAIL(GPIR_UNSUPPORTED, "unsupported combination");
+  }
+  if (rc) return rc;
+  if (!stream) CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int gpir_layout_convert(gpir_ctx* c, const uint32_t* d_in, uint32_t* d_out, uint64_t polys, void* stream) {
+  if (!c || !d_in || !d_out) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  int rc = bitrev_rows(c, d_in, d_out, (size_t)polys * c->k, s);
   if (rc) return rc;
   if (!stream) CK(cudaStreamSynchronize(s));
   return 0;

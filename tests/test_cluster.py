@@ -134,6 +134,13 @@ class _ThreadComm:
                 outer.bar.wait()
                 return out
 
+            def all_gather(self, x):
+                outer.slots[rank] = x
+                outer.bar.wait()
+                out = torch.stack([outer.slots[s] for s in range(outer.n)])
+                outer.bar.wait()
+                return out
+
         return V()
 
 
@@ -167,6 +174,136 @@ def test_row_sharded_gpu_virtual_ranks(world):
         q = torch.from_numpy(qs[own].astype(np.uint32).view(np.int32)).cuda()
         slots = np.arange(B // world, dtype=np.int32)
         outs[r] = answer_row_sharded(bes[r], comm.view(r), q, slots, d0, d1).cpu().numpy().view(np.uint32)
+        torch.cuda.synchronize()
+
+    ths = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    got = np.concatenate(outs).astype(np.uint64).reshape(B, 2, po.ring.k, po.n)
+    db = O.encode_database([r.tobytes() for r in recs], d0, d1, rb, po)
+    want = O.answer_batch(qs, np.stack([c.evks for c in clients]), np.stack([c.sk_rgsw for c in clients]), db,
+                          d0, d1, po)
+    assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------------------
+# column-sharded mode (the reference's SHARD_ALL_GATHER, src/cluster.py:350-440)
+
+class OracleColShard:
+    """Oracle compute for one column-shard rank (tests only)."""
+
+    def __init__(self, po, db_pm_cols, d0, d1, n, clients_own):
+        self.po, self.db, self.d0, self.d1, self.n = po, db_pm_cols, d0, d1, n
+        self.clients = clients_own
+        R = po.ring
+        self.ct = 2 * R.k * R.n
+
+    def _rs(self, x, *shape):
+        R = self.po.ring
+        return x.numpy().astype(np.uint64).reshape(*shape, 2, R.k, R.n)
+
+    def expand(self, q_own, _slots):
+        qs = self._rs(q_own, -1)
+        leaves = O.expand(qs, np.stack([c.evks for c in self.clients]), self.d0, self.d1, self.po)
+        rg = O.build_rgsw(leaves[:, self.d0:], np.stack([c.sk_rgsw for c in self.clients]), self.po)
+        B = len(qs)
+        rows = torch.from_numpy(leaves[:, :self.d0].reshape(B, self.d0, self.ct).astype(np.int64))
+        return rows, torch.from_numpy(rg.reshape(B, rg.shape[1], rg.shape[2], self.ct).astype(np.int64))
+
+    def rowsel_coltor(self, rows_all, rg_low):
+        R = self.po.ring
+        B = rows_all.shape[0]
+        sel = O.rowsel(self._rs(rows_all, B, self.d0), self.db, R)
+        rg = self._rs(rg_low, B, rg_low.shape[1], rg_low.shape[2])
+        out = O.coltor(sel, rg, self.po) if rg_low.shape[1] else sel[:, 0]
+        return torch.from_numpy(out.reshape(B, self.ct).astype(np.int64))
+
+    def coltor(self, parts, rg_high):
+        B = parts.shape[0]
+        out = O.coltor(self._rs(parts, B, self.n), self._rs(rg_high, B, rg_high.shape[1], rg_high.shape[2]),
+                       self.po)
+        return torch.from_numpy(out.reshape(B, self.ct).astype(np.int64))
+
+
+def _col_rank_main(rank, world, port, out_path):
+    import torch.distributed as dist
+
+    from paper_2604_04696_b200.cluster import TorchComm, answer_col_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    po = O.test_params()
+    B = 2 * world
+    recs, clients, _, qs = _material(po, B)
+    db = O.encode_database(recs, D0, D1, RB, po)               # (d1, d0, kn)
+    d1l = D1 // world
+    db_local = np.ascontiguousarray(db[rank * d1l:(rank + 1) * d1l])
+    own = slice(rank * B // world, (rank + 1) * B // world)
+    be = OracleColShard(po, db_local, D0, D1, world, clients[own])
+    q_own = torch.from_numpy(qs[own].astype(np.int64))
+    out = answer_col_sharded(be, TorchComm(), q_own, None, D0, D1)
+    np.save(out_path + f".{rank}.npy", out.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_col_sharded_gloo_matches_single_process(tmp_path):
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world = 2
+    path = str(tmp_path / "resp")
+    mp.start_processes(_col_rank_main, args=(world, port, path), nprocs=world, start_method="spawn", join=True)
+    got = np.concatenate([np.load(path + f".{r}.npy") for r in range(world)]).astype(np.uint64)
+    po = O.test_params()
+    B = 2 * world
+    recs, clients, targets, qs = _material(po, B)
+    db = O.encode_database(recs, D0, D1, RB, po)
+    want = O.answer_batch(qs, np.stack([c.evks for c in clients]), np.stack([c.sk_rgsw for c in clients]), db,
+                          D0, D1, po)
+    assert np.array_equal(got.reshape(want.shape), want)
+    for c, (i, j), ct in zip(clients, targets, want):
+        assert O.decode_plain(O.decrypt(c, ct), RB, po) == recs[i * D1 + j]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_col_sharded_gpu_virtual_ranks(world):
+    from paper_2604_04696_b200.cluster import CudaColShard, answer_col_sharded
+    from tests.helpers import to_api
+
+    po = O.default_params(plain_bits=16)
+    p = to_api(po)
+    d0, d1, rb = 16, 8, 1024
+    B = 2 * world
+    rng = np.random.default_rng(78)
+    recs = rng.integers(0, 256, size=(d0 * d1, rb), dtype=np.uint8)
+    clients = [O.client_keygen(po, d0, d1, rng) for _ in range(B)]
+    targets = [(int(rng.integers(0, d0)), int(rng.integers(0, d1))) for _ in range(B)]
+    qs = np.stack([O.client_query(c, i, j, d0, d1, rng) for c, (i, j) in zip(clients, targets)])
+    comm = _ThreadComm(world)
+    d1l = d1 // world
+    grid = recs.reshape(d0, d1, rb)
+    bes, outs = [], [None] * world
+    for r in range(world):
+        cols = np.ascontiguousarray(grid[:, r * d1l:(r + 1) * d1l]).reshape(d0 * d1l, rb)
+        be = CudaColShard(p, cols, d0, d1, rb, world, 0)
+        own = range(r * B // world, (r + 1) * B // world)
+        for s, b in enumerate(own):
+            be.put_keys(s, clients[b].evks, clients[b].sk_rgsw)
+        bes.append(be)
+
+    def run(r):
+        own = slice(r * B // world, (r + 1) * B // world)
+        q = torch.from_numpy(qs[own].astype(np.uint32).view(np.int32)).cuda()
+        slots = np.arange(B // world, dtype=np.int32)
+        outs[r] = answer_col_sharded(bes[r], comm.view(r), q, slots, d0, d1).cpu().numpy().view(np.uint32)
         torch.cuda.synchronize()
 
     ths = [threading.Thread(target=run, args=(r,)) for r in range(world)]
