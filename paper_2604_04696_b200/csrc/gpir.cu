@@ -288,6 +288,7 @@ static int fold_rows(gpir_ctx* c, const uint32_t* src, uint32_t* dst, int B, int
 // launch stream, printed to stderr at the end of each batch.
 struct StageProf {
   bool on = getenv("GPIR_STAGE_PROF") != nullptr;
+  bool fine = on && atoi(getenv("GPIR_STAGE_PROF")) >= 2;  // also between the kernels of a stage
   std::vector<cudaEvent_t> ev;
   std::vector<std::string> lab;
   size_t n = 0;
@@ -376,14 +377,17 @@ struct Engine {
     if ((rc = c->ws_coeff.ensure(cn * K * N * 4))) return rc;
     if ((rc = c->ws_dig.ensure(cn * ELL * N * 4))) return rc;
     if (mode != 3 && (rc = c->ws_dn.ensure(cn * ELL * K * N * 4))) return rc;
+    if (mode == 3 && (rc = setup_attrs())) return rc;
     for (size_t n0 = 0; n0 < nodes; n0 += cn) {
       const int nn = (int)std::min(cn, nodes - n0);
       k_op_eq_intt<LOGN, K><<<dim3(nn, K), T, 0, s>>>(state, (int)n0, k_aut, c->ws_coeff.as<u32>(), c->tb, c->tc);
       CKL();
+      if (g_sprof.fine) g_sprof.mark(s, "  eq_intt");
       const size_t tot = (size_t)nn * N;
       k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), nn,
                                                                           c->ws_dig.as<int>(), c->tb, c->cc);
       CKL();
+      if (g_sprof.fine) g_sprof.mark(s, "  eq_dcp");
       if (mode == 3) {  // hybrid: the digit NTTs stream straight into the key-switch MAC (K2)
         k_eq_nttmac<LOGN, K, ELL><<<nn * K, T, 0, s>>>(state, C, (int)n0, c->ws_dig.as<int>(), ksk, k_aut, mono,
                                                        out, Cout, c->tb, c->tc);
@@ -439,6 +443,7 @@ struct Engine {
     if ((rc = c->ws_coeff.ensure(cn * 2 * K * N * 4))) return rc;
     if ((rc = c->ws_dig.ensure(cn * 2 * ELL * N * 4))) return rc;
     if (mode != 3 && (rc = c->ws_dn.ensure(cn * 2 * ELL * K * N * 4))) return rc;
+    if (mode == 3 && (rc = setup_attrs())) return rc;
     for (size_t m0 = 0; m0 < cts; m0 += cn) {
       const int nn = (int)std::min(cn, cts - m0);
       k_op_xp_intt<LOGN, K><<<dim3(2 * nn, K), T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_coeff.as<u32>(), c->tb, c->tc);
