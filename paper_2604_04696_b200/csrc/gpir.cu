@@ -337,7 +337,7 @@ struct Engine {
 
   // op-level scratch sizing: nodes per chunk bounded by ~1 GiB
   static size_t op_chunk(size_t per_node_words) {
-    const size_t budget = (size_t)1 << 28;  // words (1 GiB)
+    const size_t budget = (size_t)1 << 29;  // words (2 GiB): a whole config-2 stage in one chunk
     return std::max<size_t>(1, budget / per_node_words);
   }
 
@@ -384,7 +384,7 @@ struct Engine {
       CKL();
       if (g_sprof.fine) g_sprof.mark(s, "  eq_intt");
       const size_t tot = (size_t)nn * N;
-      k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), nn,
+      k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot / 4 + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), nn,
                                                                           c->ws_dig.as<int>(), c->tb, c->cc);
       CKL();
       if (g_sprof.fine) g_sprof.mark(s, "  eq_dcp");
@@ -449,7 +449,7 @@ struct Engine {
       k_op_xp_intt<LOGN, K><<<dim3(2 * nn, K), T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_coeff.as<u32>(), c->tb, c->tc);
       CKL();
       const size_t tot = (size_t)2 * nn * N;
-      k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), 2 * nn,
+      k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot / 4 + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), 2 * nn,
                                                                           c->ws_dig.as<int>(), c->tb, c->cc);
       CKL();
       if (mode == 3) {
@@ -990,7 +990,7 @@ int Engine<LOGN, K, ELL>::op_digits(gpir_ctx* c, const u32* h_coeff, int32_t* h_
   cudaStream_t s = c->stream;
   CK(cudaMemcpyAsync(c->ws_io0.p, h_coeff, (size_t)polys * K * N * 4, cudaMemcpyHostToDevice, s));
   const size_t tot = (size_t)polys * N;
-  k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->ws_io0.as<u32>(), (int)polys,
+  k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot / 4 + 255) / 256), 256, 0, s>>>(c->ws_io0.as<u32>(), (int)polys,
                                                                       c->ws_io1.as<int>(), c->tb, c->cc);
   CKL();
   CK(cudaMemcpyAsync(h_dig, c->ws_io1.p, (size_t)polys * ELL * N * 4, cudaMemcpyDeviceToHost, s));

@@ -567,19 +567,28 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
 }
 
 // (2) Dcp: one thread per coefficient; coeff [polys][K][N] -> digits [polys][ELL][N].
+// Four consecutive coefficients per thread: 128-bit loads and stores keep
+// enough bytes in flight to stream at HBM rate.
 template <int LOGN, int K, int ELL>
 __global__ void k_op_dcp(const u32* __restrict__ coeff, int polys, int* __restrict__ digits, Tables tb, CrtConst cc) {
   constexpr int N = 1 << LOGN;
-  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t g = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (g >= (size_t)polys * N) return;
   const size_t p = g >> LOGN, j = g & (N - 1);
-  u32 c[K];
+  uint4 v[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) c[i] = __ldg(coeff + (p * K + i) * N + j);
-  int d[ELL];
-  dcp_coeff<K, ELL>(c, d, tb, cc);
+  for (int i = 0; i < K; ++i) v[i] = __ldg(reinterpret_cast<const uint4*>(coeff + (p * K + i) * N + j));
+  int d[4][ELL];
 #pragma unroll
-  for (int e = 0; e < ELL; ++e) digits[(p * ELL + e) * N + j] = d[e];
+  for (int t = 0; t < 4; ++t) {
+    u32 c[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) c[i] = t == 0 ? v[i].x : t == 1 ? v[i].y : t == 2 ? v[i].z : v[i].w;
+    dcp_coeff<K, ELL>(c, d[t], tb, cc);
+  }
+#pragma unroll
+  for (int e = 0; e < ELL; ++e)
+    *reinterpret_cast<int4*>(digits + (p * ELL + e) * N + j) = make_int4(d[0][e], d[1][e], d[2][e], d[3][e]);
 }
 
 // (3) digit NTT: grid (polys*(ELL-1), K): lift digit mod q_i, forward NTT
