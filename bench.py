@@ -107,6 +107,40 @@ def ncu_traffic(prefix="k_rowsel_tc"):
     return best
 
 
+def phase_rooflines(d0, d1, B, k, n, ell, phases, rs_bytes, hbm_gbs, sms=148, clk_hz=1.965e9):
+    """Per-phase roofline fractions.  The tree phases (ExpandQuery, RGSW
+    assembly, ColTor) are bound by the FMA-heavy integer pipe: a Shoup
+    butterfly is one IMAD.HI (quarter rate) + two IMADs (half rate) = 8
+    SMSP-cycles per warp, an exact 64-bit MAC one IMAD.WIDE = 4 (measured,
+    tools/micro/pipes.cu).  Algorithmic work per node / external product, with
+    the top gadget digit folded into the keys: ExpandQuery node =
+    k iNTTs + k (ell-1) digit NTTs, 2 k ell n MACs; external product = 2 k iNTTs
+    + 2 k (ell-1) digit NTTs, 4 k ell n MACs.  RowSel is bound by HBM."""
+    bfly = (n // 2) * (n.bit_length() - 1)
+    total = d0 + (d1.bit_length() - 1) * ell
+    stages = (total - 1).bit_length()
+    nodes = B * sum(min(1 << t, total) for t in range(stages))
+    xp_rgsw = B * (d1.bit_length() - 1) * ell
+    xp_col = B * (d1 - 1)
+
+    def fma_ms(units, transforms, macs):
+        cyc = units * (transforms * bfly * 8 + macs * 4) / 32
+        return cyc / (sms * 4 * clk_hz) * 1e3
+
+    eq_tr, eq_mac = k + k * (ell - 1), 2 * k * ell * n
+    xp_tr, xp_mac = 2 * k + 2 * k * (ell - 1), 4 * k * ell * n
+    out = {}
+    for name, units, tr, mac in (("ExpandQuery", nodes, eq_tr, eq_mac), ("RgswAssembly", xp_rgsw, xp_tr, xp_mac),
+                                 ("ColTor", xp_col, xp_tr, xp_mac)):
+        floor = fma_ms(units, tr, mac)
+        out[name] = {"bound": "FMA-heavy pipe (IMAD / IMAD.HI)", "floor_ms": floor,
+                     "measured_ms": phases[name], "frac": floor / phases[name] if phases[name] else None}
+    floor = rs_bytes / (hbm_gbs * 1e9) * 1e3
+    out["RowSel"] = {"bound": "HBM", "floor_ms": floor, "measured_ms": phases["RowSel"],
+                     "frac": floor / phases["RowSel"] if phases["RowSel"] else None}
+    return out
+
+
 def synthetic_material(G, params, B, stages, rng):
     """Uniform-random key and query material (all kernels are data-oblivious)."""
     b = params.basis
@@ -304,6 +338,8 @@ def run_ours(args, rank, world, local_rank):
                    "plan_legend": "per stage: o operation-level, H stage-level (digit NTT + key-switch MAC fused), "
                                   "F node-fused, S split"},
         "phases_ms": {k: float(np.mean(v)) for k, v in ph.items()},
+        "phase_roofline": phase_rooflines(d0, d1, B, params.basis.k, params.basis.n, params.gadget.ell,
+                                          {k: float(np.mean(v)) for k, v in ph.items()}, rs_bytes, hbm),
         "gpu_launches": launches * args.steps,
         "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": words * 4,
                 "d2h_bytes_per_step": words * 4},
