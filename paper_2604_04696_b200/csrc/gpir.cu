@@ -500,10 +500,10 @@ struct Engine {
       // p per staged epilogue flush: the staging buffer competes with the TMA
       // pipeline for shared memory, so the M64 x N64 tile stages 4 p (4 stages
       // in flight) rather than 8 (2 stages)
-      const int PST = (!m64 && NT == 64)                           ? 2  // only instantiation
+      const int PST = (!m64 && NT == 64)                           ? (pst_env == 2 ? 2 : 4)
                       : (pst_env == 2 || pst_env == 4 || pst_env == 8) ? pst_env
                       : m64                                      ? (NT == 64 ? 4 : 8)
-                                                                 : (NT == 64 ? 2 : 8);
+                                                                 : 4;
       const int KC = m64 ? 64 : 32;
       const int nchunks = ((int)db->d0 + KC - 1) / KC;
       const int ntiles = ((int)db->d1 + NT - 1) / NT;
@@ -557,7 +557,7 @@ struct Engine {
                                   : (PST == 8   ? k_rowsel_tc<32, true, 8, 64>
                                      : PST == 4 ? k_rowsel_tc<32, true, 4, 64>
                                                 : k_rowsel_tc<32, true, 2, 64>))
-                      : (NT == 64 ? k_rowsel_tc<64, false, 2, 32>
+                      : (NT == 64 ? (PST == 2 ? k_rowsel_tc<64, false, 2, 32> : k_rowsel_tc<64, false, 4, 32>)
                                   : (PST == 2   ? k_rowsel_tc<32, false, 2, 32>
                                      : PST == 4 ? k_rowsel_tc<32, false, 4, 32>
                                                 : k_rowsel_tc<32, false, 8, 32>));

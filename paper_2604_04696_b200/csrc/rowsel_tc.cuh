@@ -59,6 +59,21 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
+// D += A(tmem) x B(smem): the A operand read from tensor memory (M = 128 lanes, K-major)
+__device__ __forceinline__ void umma_i8_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+// 128 rows x 32 bytes from shared memory (matrix descriptor) into 8 TMEM columns
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t tmem_dst, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tmem_dst), "l"(sdesc));
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -207,11 +222,18 @@ struct TcSched {
   }
 };
 
+#ifndef TMEM_A_OK
+#define TMEM_A_OK 1
+#endif
+
 template <int TC_NT, bool M64, int TC_PST, int TC_KC>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb) {
   using Sched = TcSched<TC_PST>;
   constexpr int TC_ACC_COLS = 7 * TC_NT;
   constexpr int NBUF = (M64 || 2 * TC_ACC_COLS <= 512) ? 2 : 1;
+  // A operand from TMEM for M = 128 tiles when two accumulator buffers and two
+  // 32-column A slices fit the 512 columns
+  constexpr bool TMEM_A = TMEM_A_OK && !M64 && NBUF * TC_ACC_COLS + 64 <= 512;
   static_assert(TC_ACC_COLS <= 512, "accumulators exceed TMEM");
   extern __shared__ __align__(1024) uint8_t tc_smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -252,6 +274,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
   if (warp == 0) {  // producer: whole warp walks the schedule, one lane issues the bulk copies
     int s = 0;
     uint32_t ph = 0;
+    const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
     for (Sched sc; sc.valid(a); sc.next(a)) {
       const int p = sc.p(), nt = sc.nt;
       for (int c = 0; c < a.nchunks; ++c) {
@@ -259,8 +282,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
         if (elect_one()) {
           uint8_t* sa = stages + s * stage_bytes;
           mbar_expect_tx(&full[s], bytesA + bytesD);
-          bulk_g2s(sa, a.A8 + (((size_t)p * a.nchunks + c) * a.mtiles + sc.mt) * bytesA, bytesA, &full[s]);
-          bulk_g2s(sa + bytesA, a.D8 + (((size_t)p * a.nchunks + c) * a.ntiles + nt) * bytesD, bytesD, &full[s]);
+          const uint8_t* ga = a.A8 + (((size_t)p * a.nchunks + c) * a.mtiles + sc.mt) * bytesA;
+          const uint8_t* gd = a.D8 + (((size_t)p * a.nchunks + c) * a.ntiles + nt) * bytesD;
+          if (a.ntiles > 1) {  // A is re-read once per column tile: keep it in L2, stream D past it
+            bulk_g2s_hint(sa, ga, bytesA, &full[s], pol_keep);
+            bulk_g2s_hint(sa + bytesA, gd, bytesD, &full[s], pol_stream);
+          } else {
+            bulk_g2s(sa, ga, bytesA, &full[s]);
+            bulk_g2s(sa + bytesA, gd, bytesD, &full[s]);
+          }
         }
         __syncwarp();
         if (++s == NS) {
@@ -274,6 +304,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
     int s = 0;
     uint32_t ph = 0;
     int local = 0;
+    uint32_t ka = 0;                                        // A TMEM double-buffer index (TMEM_A)
     const uint32_t a_ks = (2u * a.RA * 16u) >> 4;         // descriptor step of one 32-byte K step
     const uint32_t a_pl = (uint32_t)(a.RA * TC_KC) >> 4;  // ... of one byte plane
     for (Sched sc; sc.valid(a); sc.next(a), ++local) {
@@ -297,17 +328,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
           const uint64_t b0 = umma_desc(sa + bytesA, TC_NT * 16, 128);
 #pragma unroll
           for (int ks = 0; ks < TC_KC / 32; ++ks) {
+            // M = 128 tiles: each A plane slice goes to TMEM once (tcgen05.cp) and
+            // feeds its four MMAs from there, so per MMA only the B tile is read
+            // from shared memory (A: 4 KiB per MMA otherwise: the SMEM-bandwidth bound)
+            const uint32_t ta = tbase + (uint32_t)(NBUF * TC_ACC_COLS + 32 * (ka & 1));
+            if constexpr (TMEM_A) {
+#pragma unroll
+              for (int sp = 0; sp < 4; ++sp)
+                tmem_cp_128x256b(ta + 8 * sp, a0 + (uint64_t)(sp * a_pl + ks * a_ks));
+            }
 #pragma unroll
             for (int sp = 0; sp < 4; ++sp) {
 #pragma unroll
               for (int tp = 0; tp < 4; ++tp) {
                 const int u = sp + tp;
                 const bool first = (ks == 0) && (sp == (u > 3 ? u - 3 : 0));  // first product into diagonal u
-                const uint64_t ad = a0 + (uint64_t)(sp * a_pl + ks * a_ks);
                 const uint64_t bd = b0 + (uint64_t)((tp * TC_NT * TC_KC + ks * 2 * TC_NT * 16) >> 4);
-                umma_i8(dcol + u * TC_NT, ad, bd, idesc, (c > 0 || !first) ? 1u : 0u);
+                const uint32_t acc = (c > 0 || !first) ? 1u : 0u;
+                if constexpr (TMEM_A) {
+                  umma_i8_ta(dcol + u * TC_NT, ta + 8 * sp, bd, idesc, acc);
+                } else {
+                  const uint64_t ad = a0 + (uint64_t)(sp * a_pl + ks * a_ks);
+                  umma_i8(dcol + u * TC_NT, ad, bd, idesc, acc);
+                }
               }
             }
+            ++ka;
           }
           umma_commit(&empty[s]);  // smem stage free once these MMAs retire
           if (c == a.nchunks - 1) umma_commit(&tfull[ab]);
