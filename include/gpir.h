@@ -68,6 +68,17 @@ typedef struct gpir_stats {
   float ms_rowsel_kernel; /* RowSel GEMM kernel alone      */
 } gpir_stats;
 
+/* Per-stage device time of the last batch (gpir_set_stage_timing on): one
+ * entry per ExpandQuery stage, RGSW assembly, RowSel (incl. the operand pack)
+ * and ColTor stage, from CUDA events on the launch stream. */
+typedef struct gpir_stage_time {
+  uint8_t phase;  /* 0 ExpandQuery, 1 RgswAssembly, 2 RowSel, 3 ColTor */
+  uint8_t mode;   /* executor mode of the stage (see header comment) */
+  uint16_t stage; /* stage index within the phase */
+  uint32_t units; /* nodes / ciphertexts / queries processed by the stage (whole batch) */
+  float ms;
+} gpir_stage_time;
+
 const char* gpir_last_error(void);
 /* byte offset of the last GPIR_PARSE_ERROR (ParseError.offset) */
 int64_t gpir_last_error_offset(void);
@@ -123,6 +134,10 @@ int gpir_answer_batch(gpir_ctx* ctx, const gpir_db* db, const uint32_t* queries,
 int gpir_answer_batch_dev(gpir_ctx* ctx, const gpir_db* db, const uint32_t* d_queries, const int32_t* key_slots,
                           uint32_t B, const uint8_t* eq_modes, uint32_t n_eq, const uint8_t* ct_modes, uint32_t n_ct,
                           uint32_t* d_responses, void* stream, gpir_stats* stats);
+
+int gpir_set_stage_timing(gpir_ctx* ctx, int on);
+/* copies up to cap entries of the last timed batch; returns the entry count (>= 0) */
+int gpir_stage_times(gpir_ctx* ctx, gpir_stage_time* out, uint32_t cap);
 
 /* Built-in B200 hybrid plan (per-stage op/fused choice) for a geometry/batch. */
 int gpir_plan(gpir_ctx* ctx, uint32_t d0, uint32_t d1, uint32_t B, uint8_t* eq_modes, uint32_t n_eq,

@@ -28,6 +28,11 @@ class GpirStats(C.Structure):
     ]
 
 
+class GpirStageTime(C.Structure):
+    _fields_ = [("phase", C.c_uint8), ("mode", C.c_uint8), ("stage", C.c_uint16), ("units", C.c_uint32),
+                ("ms", C.c_float)]
+
+
 # name -> (restype, argtypes)
 _SIGS = {
     "gpir_last_error": (C.c_char_p, []),
@@ -60,6 +65,8 @@ _SIGS = {
     "gpir_sharded_rgsw": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
     "gpir_layout_convert": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "gpir_last_error_offset": (C.c_int64, []),
+    "gpir_set_stage_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "gpir_stage_times": (C.c_int, [C.c_void_p, C.POINTER(GpirStageTime), C.c_uint32]),
     "gpir_db_load": (C.c_void_p, [C.c_void_p, C.c_char_p, C.c_uint32, _u32p, _u32p, _u32p, _u32p]),
     "gpir_db_save": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_uint32, C.c_uint32]),
     "gpir_wire_parse_header": (C.c_int, [C.c_void_p, C.c_size_t, _u32p, C.POINTER(C.c_uint64)]),

@@ -99,6 +99,8 @@ struct gpir_ctx {
   CrtConst cc{};
   TwConst tc{};
   FoldConst fc{};
+  int stage_timing = 0;
+  std::vector<gpir_stage_time> last_stages;
   DevBuf tw_fwd, tw_inv, mono;
   // key pool
   uint32_t key_slots = 0, key_stages = 0;
@@ -287,31 +289,52 @@ static int fold_rows(gpir_ctx* c, const uint32_t* src, uint32_t* dst, int B, int
 // Per-stage device timing for plan tuning (GPIR_STAGE_PROF=1): events on the
 // launch stream, printed to stderr at the end of each batch.
 struct StageProf {
-  bool on = getenv("GPIR_STAGE_PROF") != nullptr;
-  bool fine = on && atoi(getenv("GPIR_STAGE_PROF")) >= 2;  // also between the kernels of a stage
+  bool env = getenv("GPIR_STAGE_PROF") != nullptr;
+  bool fine = env && atoi(getenv("GPIR_STAGE_PROF")) >= 2;  // also between the kernels of a stage
+  bool on = false;
   std::vector<cudaEvent_t> ev;
   std::vector<std::string> lab;
+  std::vector<gpir_stage_time> info;
   size_t n = 0;
-  void mark(cudaStream_t s, const std::string& l) {
+  void begin(bool ctx_on) {
+    on = env || ctx_on;
+    n = 0;
+  }
+  void mark(cudaStream_t s, const std::string& l, int phase = -1, int stage = 0, int mode = 0, uint32_t units = 0) {
     if (!on) return;
     if (n == ev.size()) {
       cudaEvent_t e;
       cudaEventCreate(&e);
       ev.push_back(e);
       lab.emplace_back();
+      info.emplace_back();
     }
     lab[n] = l;
+    info[n] = gpir_stage_time{(uint8_t)(phase < 0 ? 255 : phase), (uint8_t)mode, (uint16_t)stage, units, 0.f};
     cudaEventRecord(ev[n++], s);
   }
-  void flush() {
+  // per-interval times; phase entries (phase != 255) are returned, labels printed under GPIR_STAGE_PROF
+  void flush(std::vector<gpir_stage_time>* out) {
     if (!on || n < 2) return;
     cudaEventSynchronize(ev[n - 1]);
+    if (out) out->clear();
+    float acc = 0;
     for (size_t i = 1; i < n; ++i) {
       float ms = 0;
       cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
-      fprintf(stderr, "[stage prof] %-16s %8.3f ms\n", lab[i].c_str(), ms);
+      if (env) fprintf(stderr, "[stage prof] %-16s %8.3f ms\n", lab[i].c_str(), ms);
+      acc += ms;
+      if (info[i].phase != 255) {  // fine-grained sub-marks fold into the next stage entry
+        if (out) {
+          gpir_stage_time t = info[i];
+          t.ms = acc;
+          out->push_back(t);
+        }
+        acc = 0;
+      }
     }
     n = 0;
+    on = false;
   }
 };
 static thread_local StageProf g_sprof;
@@ -647,7 +670,7 @@ struct Engine {
       const int mode = (eq_modes && t < n_eq) ? eq_modes[t] : default_mode(B * C);
       int rc = expand_stage(c, cur, B, C, nxt, Cout, (int)t, evk_rows(c, (int)t, kslot), mode, s, launches);
       if (rc) return rc;
-      g_sprof.mark(s, "eq" + std::to_string(t) + " " + "oFSH"[mode & 3]);
+      g_sprof.mark(s, "eq" + std::to_string(t) + " " + "oFSH"[mode & 3], 0, (int)t, mode, (uint32_t)(B * C));
       std::swap(cur, nxt);
     }
     *leaves_out = cur;
@@ -692,6 +715,7 @@ struct Engine {
     uint32_t launches = 0;
     int rc;
     if (st) CK(cudaEventRecord(c->ev[1], s));
+    g_sprof.begin(c->stage_timing != 0);
     g_sprof.mark(s, "start");
     u32* leaves = nullptr;
     if ((rc = expand_all(c, B, total, eq_modes, n_eq, kslot, &leaves, s, &launches))) return rc;
@@ -705,12 +729,12 @@ struct Engine {
         return rc;
     }
     if (st) CK(cudaEventRecord(c->ev[3], s));
-    g_sprof.mark(s, "rgsw");
+    g_sprof.mark(s, "rgsw", 1, 0, xp_default((size_t)B * bits_tree * ELL), (uint32_t)(B * bits_tree * ELL));
     if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches,
                      st ? c->ev[11] : nullptr)))
       return rc;
     if (st) CK(cudaEventRecord(c->ev[4], s));
-    g_sprof.mark(s, "rowsel+pack");
+    g_sprof.mark(s, "rowsel+pack", 2, 0, 0, (uint32_t)B);
     // ColTor (src/protocol.py:542-573): LSB-first pairs
     if ((rc = fold_coltor(c, B, bits, c->ws_arows.as<u32>(), (size_t)bits_tree * ELL * CT, leaves + (size_t)d0 * CT,
                           (size_t)total * CT, s)))
@@ -723,11 +747,11 @@ struct Engine {
       const int mode = (ct_modes && j < n_ct) ? ct_modes[j] : xp_default((size_t)B * C / 2);
       u32* dst = bufs[j & 1];
       if ((rc = ext_product(c, cur, (size_t)C, B, C / 2, 1, dst, (size_t)C / 2, r, mode, s, &launches))) return rc;
-      g_sprof.mark(s, "coltor" + std::to_string(j) + " " + "oFSH"[mode & 3]);
+      g_sprof.mark(s, "coltor" + std::to_string(j) + " " + "oFSH"[mode & 3], 3, (int)j, mode, (uint32_t)(B * C / 2));
       cur = dst;
     }
     if (st) CK(cudaEventRecord(c->ev[5], s));
-    g_sprof.flush();
+    g_sprof.flush(&c->last_stages);
     *result = cur;
     if (leaves_out) *leaves_out = leaves;
     if (st) st->launches += launches;
@@ -1543,6 +1567,21 @@ int gpir_answer_batch(gpir_ctx* c, const gpir_db* db, const uint32_t* queries, c
     cudaEventElapsedTime(&stats->ms_d2h, c->ev[9], c->ev[10]);
   }
   return 0;
+}
+
+int gpir_set_stage_timing(gpir_ctx* c, int on) {
+  if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->stage_timing = on ? 1 : 0;
+  return 0;
+}
+
+int gpir_stage_times(gpir_ctx* c, gpir_stage_time* out, uint32_t cap) {
+  if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  const uint32_t m = std::min<uint32_t>(cap, (uint32_t)c->last_stages.size());
+  for (uint32_t i = 0; i < m && out; ++i) out[i] = c->last_stages[i];
+  return (int)c->last_stages.size();
 }
 
 int gpir_plan(gpir_ctx* c, uint32_t d0, uint32_t d1, uint32_t B, uint8_t* eq_modes, uint32_t n_eq, uint8_t* ct_modes,

@@ -182,3 +182,103 @@ class BatchCollector:
             replies[i](m)
         self.batches_served += 1
         self.batch_sizes.append(len(good))
+
+
+# ---------------------------------------------------------------------------
+# benchmark harness (latpir.server.run_bench / BenchReport, src/server.py:371-455)
+
+_PHASES = ("ExpandQuery", "RgswAssembly", "RowSel", "ColTor")
+_MODES = {0: "op", 1: "stage", 2: "split", 3: "stage"}
+
+
+@dataclass
+class BenchReport:
+    """Same fields and text/CSV formats as the reference's BenchReport; the
+    per-stage rows are measured on the GPU (CUDA events per stage) and
+    `allocator_traffic_bytes` is the device workspace of the batch."""
+
+    batch: int
+    batches: int
+    phase_ms_per_query: dict
+    qps: float
+    allocator_traffic_bytes: int
+    stage_rows: list  # (phase, stage, nodes, working_set, mode, amortized_ms)
+    plan_text: str
+    ledger_text: str = ""
+
+    def to_text(self) -> str:
+        lines = [f"batch\t{self.batch}", f"batches\t{self.batches}", f"qps\t{self.qps:.3f}",
+                 f"allocator_traffic_bytes\t{self.allocator_traffic_bytes}"]
+        for phase, ms in self.phase_ms_per_query.items():
+            lines.append(f"amortized_ms\t{phase}\t{ms:.3f}")
+        lines.append("-- plan --")
+        lines.append(self.plan_text.rstrip("\n"))
+        if self.ledger_text:
+            lines.append("-- comm --")
+            lines.append(self.ledger_text.rstrip("\n"))
+        return "\n".join(lines) + "\n"
+
+    def stage_csv(self) -> str:
+        rows = ["phase,stage,nodes,working_set_bytes,mode,amortized_ms"]
+        for phase, stage, nodes, ws, mode, ms in self.stage_rows:
+            rows.append(f"{phase},{stage},{nodes},{ws},{mode},{ms:.4f}")
+        return "\n".join(rows) + "\n"
+
+
+def run_bench(db, params, batches: int, batch: int = 32, seed: int = 1234, hw=None) -> BenchReport:
+    """Serve `batches` seeded batches of `batch` queries and report amortized
+    per-phase and per-stage costs (src/server.py:409-455).  Key and query
+    material is uniform random (the kernels are data-oblivious), one key set per
+    query slot; timing is device time from CUDA events."""
+    import ctypes as C
+
+    from . import _native as nat
+    from .planner import HardwareModel, Phase, build_plan, working_set
+
+    hw = hw or HardwareModel.b200()
+    rng = np.random.default_rng(seed)
+    b = params.basis
+    k, n, ell = b.k, b.n, params.gadget.ell
+    cfg = db.config
+    stages = planner.num_expand_stages(planner.expansion_leaves(cfg.d0, cfg.d1, ell))
+    qs = np.array([m.q for m in b.moduli], dtype=np.uint64)[:, None]
+
+    def uni(*shape):
+        return (rng.integers(0, 1 << 62, size=shape + (k, n), dtype=np.uint64) % qs).astype(np.uint32)
+
+    from .wire import RawKeys
+
+    keys = {c: RawKeys(n, uni(stages, ell, 2), uni(2 * ell, 2)) for c in range(batch)}
+    ddb = protocol._device_db(db, params)
+    ctx = ddb.ctx
+    nat.check(ctx.lib.gpir_set_stage_timing(ctx.h, 1), "stage timing")
+    plan = build_plan(cfg, params, batch, hw)
+    phase_tot = {p: 0.0 for p in _PHASES}
+    stage_acc: dict = {}
+    wall = 0.0
+    buf = (nat.GpirStageTime * 64)()
+    try:
+        for _ in range(batches):
+            qarr = uni(batch, 2)
+            t0 = time.perf_counter()
+            protocol.answer_raw(qarr, list(range(batch)), keys, db, params, hw=hw, plan=plan)
+            wall += time.perf_counter() - t0
+            cnt = ctx.lib.gpir_stage_times(ctx.h, buf, len(buf))
+            for e in buf[:min(cnt, len(buf))]:
+                phase = _PHASES[e.phase]
+                phase_tot[phase] += e.ms / 1e3
+                if phase == "RowSel":
+                    continue
+                ph = Phase.EXPAND_QUERY if phase == "ExpandQuery" else Phase.COL_TOR
+                ws = working_set(ph, e.stage, batch, params, cfg) if phase != "RgswAssembly" else 0
+                key = (phase, e.stage, e.units // batch if phase != "RgswAssembly" else e.units, ws,
+                       _MODES.get(e.mode, "op"))
+                stage_acc.setdefault(key, []).append(e.ms / 1e3)
+    finally:
+        ctx.lib.gpir_set_stage_timing(ctx.h, 0)
+    nq = batches * batch
+    return BenchReport(
+        batch=batch, batches=batches, phase_ms_per_query={p: t / nq * 1e3 for p, t in phase_tot.items()},
+        qps=nq / wall if wall else 0.0, allocator_traffic_bytes=int(ddb.device_bytes),
+        stage_rows=sorted(key + (sum(v) / nq * 1e3,) for key, v in stage_acc.items()),
+        plan_text=plan.to_text() if hasattr(plan, "to_text") else str(plan))
