@@ -408,7 +408,7 @@ struct Engine {
       if (g_sprof.fine) g_sprof.mark(s, "  eq_intt");
       const size_t tot = (size_t)nn * N;
       k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot / 4 + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), nn,
-                                                                          c->ws_dig.as<int>(), c->tb, c->cc);
+                                                                          c->ws_dig.as<int>(), c->tb, c->cc, ELL - 1);
       CKL();
       if (g_sprof.fine) g_sprof.mark(s, "  eq_dcp");
       if (mode == 3) {  // hybrid: the digit NTTs stream straight into the key-switch MAC (K2)
@@ -473,7 +473,7 @@ struct Engine {
       CKL();
       const size_t tot = (size_t)2 * nn * N;
       k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot / 4 + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), 2 * nn,
-                                                                          c->ws_dig.as<int>(), c->tb, c->cc);
+                                                                          c->ws_dig.as<int>(), c->tb, c->cc, ELL - 1);
       CKL();
       if (mode == 3) {
         k_xp_nttmac<LOGN, K, ELL><<<nn * K, T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_dig.as<int>(), rows, out,
@@ -1015,7 +1015,7 @@ int Engine<LOGN, K, ELL>::op_digits(gpir_ctx* c, const u32* h_coeff, int32_t* h_
   CK(cudaMemcpyAsync(c->ws_io0.p, h_coeff, (size_t)polys * K * N * 4, cudaMemcpyHostToDevice, s));
   const size_t tot = (size_t)polys * N;
   k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot / 4 + 255) / 256), 256, 0, s>>>(c->ws_io0.as<u32>(), (int)polys,
-                                                                      c->ws_io1.as<int>(), c->tb, c->cc);
+                                                                      c->ws_io1.as<int>(), c->tb, c->cc, ELL);
   CKL();
   CK(cudaMemcpyAsync(h_dig, c->ws_io1.p, (size_t)polys * ELL * N * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));

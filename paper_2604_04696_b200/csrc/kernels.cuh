@@ -569,8 +569,10 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
 // (2) Dcp: one thread per coefficient; coeff [polys][K][N] -> digits [polys][ELL][N].
 // Four consecutive coefficients per thread: 128-bit loads and stores keep
 // enough bytes in flight to stream at HBM rate.
+// ndig < ELL skips the top digits (the pipeline never reads the folded one)
 template <int LOGN, int K, int ELL>
-__global__ void k_op_dcp(const u32* __restrict__ coeff, int polys, int* __restrict__ digits, Tables tb, CrtConst cc) {
+__global__ void k_op_dcp(const u32* __restrict__ coeff, int polys, int* __restrict__ digits, Tables tb, CrtConst cc,
+                         int ndig) {
   constexpr int N = 1 << LOGN;
   const size_t g = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (g >= (size_t)polys * N) return;
@@ -588,7 +590,8 @@ __global__ void k_op_dcp(const u32* __restrict__ coeff, int polys, int* __restri
   }
 #pragma unroll
   for (int e = 0; e < ELL; ++e)
-    *reinterpret_cast<int4*>(digits + (p * ELL + e) * N + j) = make_int4(d[0][e], d[1][e], d[2][e], d[3][e]);
+    if (e < ndig)
+      *reinterpret_cast<int4*>(digits + (p * ELL + e) * N + j) = make_int4(d[0][e], d[1][e], d[2][e], d[3][e]);
 }
 
 // (3) digit NTT: grid (polys*(ELL-1), K): lift digit mod q_i, forward NTT
