@@ -227,10 +227,17 @@ def run_ours(args, rank, world, local_rank):
     lib = ctx.lib
     total = G.planner.expansion_leaves(d0, d1, params.gadget.ell)
     stages = G.planner.num_expand_stages(total)
-    evks, rgsw, queries = synthetic_material(G, params, B, stages, rng)
-    for b in range(B):
-        nat.check(lib.gpir_keys_put(ctx.h, b, nat.ptr(np.ascontiguousarray(evks[b])), stages,
-                                    nat.ptr(np.ascontiguousarray(rgsw[b]))), "keys")
+    if args.material == "gpu":  # B distinct real clients: keys and queries generated on the GPU
+        from paper_2604_04696_b200 import client
+
+        coords = [(int(rng.integers(0, d0)), int(rng.integers(0, d1))) for _ in range(B)]
+        queries = np.concatenate([client.queries(ctx, params, client.keygen(ctx, params, b, d0, d1, seed=7000 + b),
+                                                 d0, d1, [coords[b]], seed=9000 + b) for b in range(B)])
+    else:
+        evks, rgsw, queries = synthetic_material(G, params, B, stages, rng)
+        for b in range(B):
+            nat.check(lib.gpir_keys_put(ctx.h, b, nat.ptr(np.ascontiguousarray(evks[b])), stages,
+                                        nat.ptr(np.ascontiguousarray(rgsw[b]))), "keys")
     slots = np.arange(B, dtype=np.int32)
     words = queries.size
     d_q = torch.from_numpy(queries.view(np.int32).reshape(-1)).to(f"cuda:{dev}")
@@ -328,7 +335,9 @@ def run_ours(args, rank, world, local_rank):
         "metric": "PIR queries/sec (batched)", "value": qps, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 (mod-q, 64-bit lazy products)",
-        "data": "synthetic (random records, uniform-random key/query material)",
+        "data": ("synthetic random records; B distinct clients' keys and queries generated on the GPU "
+                 "(paper_2604_04696_b200.client)" if args.material == "gpu" else
+                 "synthetic (random records, uniform-random key/query material)"),
         "config": {"workload": desc, "d0": d0, "d1": d1, "global_batch": B * world, "per_gpu_batch": B,
                    "record_bytes": rb, "plain_bits": pb, "encoded_db_bytes": d0 * d1 * KN * 4,
                    "l2": f"inputs larger than L2 ({d0 * d1 * KN * 4 >> 30} GiB DB streamed by RowSel every step)",
@@ -444,6 +453,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--modes", default="", help='"fused", "op", or an explicit plan "EQ/CT" (o/F/S/H per stage)')
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--material", default="gpu", choices=["gpu", "uniform"],
+                    help="client keys/queries: real ones generated on the GPU, or uniform-random residues")
     ap.add_argument("--strategy", default="replica", choices=["replica", "rowshard", "colshard"],
                     help="multi-GPU mode: replica (DB copy + own batch per GPU), rowshard (north-star DB row "
                          "shards, modular-add combine) or colshard (DB column shards, all-gather)")

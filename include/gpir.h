@@ -123,6 +123,20 @@ size_t gpir_db_bytes(const gpir_db* db);
 int gpir_keys_put(gpir_ctx* ctx, int slot, const uint32_t* evks, uint32_t stages, const uint32_t* sk_rgsw);
 int gpir_keys_drop(gpir_ctx* ctx, int slot);
 
+/* ---- client-side material on the GPU (benchmark input factory; src/he.py:220-271,
+ * 423-431, 487-515, src/protocol.py:240-281) ----
+ * keygen samples a ternary secret and encrypts the `stages` expansion keys and
+ * RGSW(s) with errors of the given bound (a counter-based RNG keyed by seed, so
+ * samples differ from numpy's, distributions and equations do not), installs
+ * them in key slot `slot`, and returns the secret's coefficients (int8, n) for
+ * client-side decryption.  queries encrypts (i*, j*) pairs under that secret:
+ * queries_out[count][2][k][n] host, natural order. */
+int gpir_client_keygen(gpir_ctx* ctx, int slot, uint32_t stages, uint64_t seed, uint32_t error_bound,
+                       int8_t* secret_out);
+int gpir_client_queries(gpir_ctx* ctx, const int8_t* secret, uint32_t plain_bits, uint32_t error_bound, uint32_t d0,
+                        uint32_t d1, const uint32_t* i_star, const uint32_t* j_star, uint32_t count, uint64_t seed,
+                        uint32_t* queries_out);
+
 /* Full server pipeline for B queries (src/protocol.py:635-682).
  * queries[B][2][k][n] host; key_slots[B]; modes: one byte per ExpandQuery stage
  * (n_eq) and per ColTor stage (n_ct), or NULL for the built-in B200 plan;

@@ -66,6 +66,9 @@ _SIGS = {
     "gpir_layout_convert": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "gpir_last_error_offset": (C.c_int64, []),
     "gpir_set_stage_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "gpir_client_keygen": (C.c_int, [C.c_void_p, C.c_int, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p]),
+    "gpir_client_queries": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u32p,
+                                      _u32p, C.c_uint32, C.c_uint64, _u32p]),
     "gpir_stage_times": (C.c_int, [C.c_void_p, C.POINTER(GpirStageTime), C.c_uint32]),
     "gpir_db_load": (C.c_void_p, [C.c_void_p, C.c_char_p, C.c_uint32, _u32p, _u32p, _u32p, _u32p]),
     "gpir_db_save": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_uint32, C.c_uint32]),

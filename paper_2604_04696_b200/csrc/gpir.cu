@@ -17,6 +17,7 @@
 #include "kernels.cuh"
 #include "rowsel_tc.cuh"
 #include "stage_kernels.cuh"
+#include "client.cuh"
 
 // hybrid planner thresholds (nodes / ciphertexts per stage, whole batch)
 static constexpr size_t kEqStageNodes = 2048;
@@ -100,6 +101,7 @@ struct gpir_ctx {
   TwConst tc{};
   FoldConst fc{};
   int stage_timing = 0;
+  uint32_t error_bound = 16;
   std::vector<gpir_stage_time> last_stages;
   DevBuf tw_fwd, tw_inv, mono;
   // key pool
@@ -959,6 +961,10 @@ struct Engine {
                              u32* h_out);
   static int op_xp(gpir_ctx* c, const u32* h_cts, int B, int M, int pairs, const u32* h_rows, int mode, u32* h_out);
   static int op_rowsel(gpir_ctx* c, const u32* h_rows, int B, gpir_db* db, u32* h_out);
+  // client-side material (client.cuh)
+  static int client_keygen(gpir_ctx* c, int slot, uint32_t stages, uint64_t seed, int8_t* h_secret);
+  static int client_queries(gpir_ctx* c, const int8_t* h_secret, uint32_t plain_bits, uint32_t d0, uint32_t d1,
+                            const uint32_t* istar, const uint32_t* jstar, uint32_t count, uint64_t seed, u32* h_out);
 };
 
 // plain NTT rows kernels for the parity entry point
@@ -1002,6 +1008,97 @@ int Engine<LOGN, K, ELL>::op_ntt(gpir_ctx* c, const u32* h_in, u32* h_out, uint3
     if ((rc = bitrev_rows(c, c->ws_io1.as<u32>(), c->ws_io0.as<u32>(), rows, s))) return rc;
     CK(cudaMemcpyAsync(h_out, c->ws_io0.p, words * 4, cudaMemcpyDeviceToHost, s));
   }
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+extern "C" {
+static int install_keys_brv(gpir_ctx* c, int slot, const uint32_t* d_evks, uint32_t stages, const uint32_t* d_rgsw);
+}
+
+// z^i mod q_i for i < ell, [ell][K]
+static std::vector<uint32_t> zpow_table(const gpir_ctx* c) {
+  std::vector<uint32_t> z((size_t)c->ell * c->k);
+  for (uint32_t i = 0; i < c->ell; ++i)
+    for (uint32_t l = 0; l < c->k; ++l)
+      z[(size_t)i * c->k + l] = (uint32_t)powmod(powmod(2, c->z_bits, c->q[l]), i, c->q[l]);
+  return z;
+}
+
+template <int LOGN, int K, int ELL>
+int Engine<LOGN, K, ELL>::client_keygen(gpir_ctx* c, int slot, uint32_t stages, uint64_t seed, int8_t* h_secret) {
+  cudaStream_t s = c->stream;
+  const size_t rows = (size_t)stages * ELL + 2 * ELL;
+  DevBuf sc, snat, sbrv, zp, ph, ct;
+  int rc;
+  if ((rc = sc.ensure(N)) || (rc = snat.ensure((size_t)K * N * 4)) || (rc = sbrv.ensure((size_t)K * N * 4)) ||
+      (rc = zp.ensure((size_t)ELL * K * 4)) || (rc = ph.ensure(rows * K * N * 4)) || (rc = ct.ensure(rows * CT * 4)))
+    return rc;
+  k_client_secret<<<(N + 255) / 256, 256, 0, s>>>(seed, N, K, sc.as<int8_t>(), snat.as<u32>(), c->tb);
+  CKL();
+  k_ntt_rows<LOGN, K><<<K, T, 0, s>>>(snat.as<u32>(), sbrv.as<u32>(), 0, c->tb, c->tc);
+  CKL();
+  const std::vector<uint32_t> z = zpow_table(c);
+  CK(cudaMemcpyAsync(zp.p, z.data(), z.size() * 4, cudaMemcpyHostToDevice, s));
+  const size_t tot = rows * K * N;
+  k_client_key_phases<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(sbrv.as<u32>(), LOGN, K, (int)stages, ELL,
+                                                                    zp.as<u32>(), ph.as<u32>(), c->tb);
+  CKL();
+  k_client_encrypt<LOGN, K><<<dim3((unsigned)rows, K), T, 0, s>>>(seed, 0, ph.as<u32>(), sbrv.as<u32>(), ct.as<u32>(),
+                                                                 (int)c->error_bound, c->tb, c->tc);
+  CKL();
+  if ((rc = install_keys_brv(c, slot, ct.as<u32>(), stages, ct.as<u32>() + (size_t)stages * ELL * CT))) return rc;
+  if (h_secret) CK(cudaMemcpy(h_secret, sc.p, N, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+template <int LOGN, int K, int ELL>
+int Engine<LOGN, K, ELL>::client_queries(gpir_ctx* c, const int8_t* h_secret, uint32_t plain_bits, uint32_t d0,
+                                         uint32_t d1, const uint32_t* istar, const uint32_t* jstar, uint32_t count,
+                                         uint64_t seed, u32* h_out) {
+  cudaStream_t s = c->stream;
+  const uint32_t total = leaves_of(d0, d1, ELL), stages = stages_of(total), bits = ilog2(d1);
+  if (total > (uint32_t)N) FAIL(GPIR_INVALID_ARGUMENT, "expansion needs more slots than the ring has");
+  if (!plain_bits || plain_bits > 32) FAIL(GPIR_INVALID_ARGUMENT, "plain modulus must be 2^1 .. 2^32");
+  // payload (src/protocol.py:252-281): Delta / 2^stages at i*, z^dig / 2^stages at the column-bit slots
+  u128 Q = 1;
+  for (uint32_t l = 0; l < (uint32_t)K; ++l) Q *= c->q[l];
+  const u128 delta = Q >> plain_bits;
+  const std::vector<uint32_t> z = zpow_table(c);
+  std::vector<uint32_t> pay((size_t)count * K * N, 0);
+  for (uint32_t b = 0; b < count; ++b) {
+    if (istar[b] >= d0 || jstar[b] >= d1) FAIL(GPIR_INVALID_ARGUMENT, "query index out of range");
+    for (uint32_t l = 0; l < (uint32_t)K; ++l) {
+      const uint64_t q = c->q[l];
+      const uint64_t inv = powmod(powmod(2, stages, q), q - 2, q);
+      uint32_t* row = pay.data() + ((size_t)b * K + l) * N;
+      row[istar[b]] = (uint32_t)((uint64_t)(delta % q) * inv % q);
+      for (uint32_t bit = 0; bit < bits; ++bit)
+        if ((jstar[b] >> bit) & 1)
+          for (uint32_t dg = 0; dg < (uint32_t)ELL; ++dg)
+            row[d0 + bit * ELL + dg] = (uint32_t)((uint64_t)z[(size_t)dg * K + l] * inv % q);
+    }
+  }
+  DevBuf sc, snat, sbrv, pnat, pbrv, ct, nat;
+  int rc;
+  const size_t pw = (size_t)count * K * N;
+  if ((rc = sc.ensure(N)) || (rc = snat.ensure((size_t)K * N * 4)) || (rc = sbrv.ensure((size_t)K * N * 4)) ||
+      (rc = pnat.ensure(pw * 4)) || (rc = pbrv.ensure(pw * 4)) || (rc = ct.ensure((size_t)count * CT * 4)) ||
+      (rc = nat.ensure((size_t)count * CT * 4)))
+    return rc;
+  CK(cudaMemcpyAsync(sc.p, h_secret, N, cudaMemcpyHostToDevice, s));
+  k_client_lift<<<(N + 255) / 256, 256, 0, s>>>(sc.as<int8_t>(), N, K, snat.as<u32>(), c->tb);
+  CKL();
+  k_ntt_rows<LOGN, K><<<K, T, 0, s>>>(snat.as<u32>(), sbrv.as<u32>(), 0, c->tb, c->tc);
+  CKL();
+  CK(cudaMemcpyAsync(pnat.p, pay.data(), pw * 4, cudaMemcpyHostToDevice, s));
+  k_ntt_rows<LOGN, K><<<(unsigned)(count * K), T, 0, s>>>(pnat.as<u32>(), pbrv.as<u32>(), 0, c->tb, c->tc);
+  CKL();
+  k_client_encrypt<LOGN, K><<<dim3(count, K), T, 0, s>>>(seed, 1u << 20, pbrv.as<u32>(), sbrv.as<u32>(), ct.as<u32>(),
+                                                        (int)c->error_bound, c->tb, c->tc);
+  CKL();
+  if ((rc = bitrev_rows(c, ct.as<u32>(), nat.as<u32>(), (size_t)count * 2 * K, s))) return rc;
+  CK(cudaMemcpyAsync(h_out, nat.p, (size_t)count * CT * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return 0;
 }
@@ -1441,6 +1538,61 @@ void gpir_db_destroy(gpir_ctx* c, gpir_db* db) {
 
 size_t gpir_db_bytes(const gpir_db* db) { return db ? db->data.bytes : 0; }
 
+// grow the key pools (slots x max stages), preserving existing keys; caller holds c->mu
+static int ensure_key_pool(gpir_ctx* c, int slot, uint32_t stages) {
+  const size_t CT = c->ct_words();
+  const size_t ell = c->ell;
+  int rc;
+  const uint32_t want_slots = std::max<uint32_t>(c->key_slots, (uint32_t)slot + 1);
+  const uint32_t want_stages = std::max<uint32_t>(c->key_stages, std::max<uint32_t>(stages, 1));
+  if (want_slots == c->key_slots && want_stages == c->key_stages) return 0;
+  const uint32_t ns = std::max<uint32_t>(want_slots, c->key_slots ? 2 * c->key_slots : 4);
+  DevBuf ne, nr;
+  if ((rc = ne.ensure((size_t)ns * want_stages * ell * CT * 4))) return rc;
+  if ((rc = nr.ensure((size_t)ns * 2 * ell * CT * 4))) return rc;
+  for (uint32_t sl = 0; sl < c->key_slots; ++sl) {
+    if (c->slot_stages[sl] > 0)
+      CK(cudaMemcpyAsync(ne.as<u32>() + (size_t)sl * want_stages * ell * CT,
+                         c->evk_pool.as<u32>() + (size_t)sl * c->key_stages * ell * CT,
+                         (size_t)c->slot_stages[sl] * ell * CT * 4, cudaMemcpyDeviceToDevice, c->stream));
+    if (c->slot_rgsw[sl])
+      CK(cudaMemcpyAsync(nr.as<u32>() + (size_t)sl * 2 * ell * CT, c->rgsw_pool.as<u32>() + (size_t)sl * 2 * ell * CT,
+                         2 * ell * CT * 4, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  c->evk_pool.release();
+  c->rgsw_pool.release();
+  c->evk_pool = ne;
+  c->rgsw_pool = nr;
+  ne.p = nullptr;
+  nr.p = nullptr;
+  c->slot_stages.resize(ns, -1);
+  c->slot_rgsw.resize(ns, 0);
+  c->key_slots = ns;
+  c->key_stages = want_stages;
+  return 0;
+}
+
+// install device key rows in internal (brv) order into slot: fold into the pool
+static int install_keys_brv(gpir_ctx* c, int slot, const uint32_t* d_evks, uint32_t stages, const uint32_t* d_rgsw) {
+  const size_t CT = c->ct_words(), ell = c->ell;
+  int rc;
+  if ((rc = ensure_key_pool(c, slot, stages))) return rc;
+  if (stages) {
+    u32* dst = c->evk_pool.as<u32>() + (size_t)slot * c->key_stages * ell * CT;
+    if ((rc = fold_rows(c, d_evks, dst, 1, (int)stages, 0, ell * CT, 0, ell * CT, c->stream))) return rc;
+  }
+  c->slot_rgsw[slot] = 0;
+  if (d_rgsw) {
+    u32* dst = c->rgsw_pool.as<u32>() + (size_t)slot * 2 * ell * CT;
+    if ((rc = fold_rows(c, d_rgsw, dst, 1, 2, 0, ell * CT, 0, ell * CT, c->stream))) return rc;
+    c->slot_rgsw[slot] = 1;
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  c->slot_stages[slot] = (int)stages;
+  return 0;
+}
+
 int gpir_keys_put(gpir_ctx* c, int slot, const uint32_t* evks, uint32_t stages, const uint32_t* sk_rgsw) {
   if (!c || slot < 0 || (stages && !evks)) FAIL(GPIR_INVALID_ARGUMENT, "invalid key upload");
   std::lock_guard<std::mutex> lk(c->mu);
@@ -1448,57 +1600,59 @@ int gpir_keys_put(gpir_ctx* c, int slot, const uint32_t* evks, uint32_t stages, 
   const size_t CT = c->ct_words();
   const size_t ell = c->ell;
   int rc;
-  // grow the pools (slots x max stages), preserving existing keys
-  const uint32_t want_slots = std::max<uint32_t>(c->key_slots, (uint32_t)slot + 1);
-  const uint32_t want_stages = std::max<uint32_t>(c->key_stages, std::max<uint32_t>(stages, 1));
-  if (want_slots != c->key_slots || want_stages != c->key_stages) {
-    const uint32_t ns = std::max<uint32_t>(want_slots, c->key_slots ? 2 * c->key_slots : 4);
-    DevBuf ne, nr;
-    if ((rc = ne.ensure((size_t)ns * want_stages * ell * CT * 4))) return rc;
-    if ((rc = nr.ensure((size_t)ns * 2 * ell * CT * 4))) return rc;
-    for (uint32_t sl = 0; sl < c->key_slots; ++sl) {
-      if (c->slot_stages[sl] > 0)
-        CK(cudaMemcpyAsync(ne.as<u32>() + (size_t)sl * want_stages * ell * CT,
-                           c->evk_pool.as<u32>() + (size_t)sl * c->key_stages * ell * CT,
-                           (size_t)c->slot_stages[sl] * ell * CT * 4, cudaMemcpyDeviceToDevice, c->stream));
-      if (c->slot_rgsw[sl])
-        CK(cudaMemcpyAsync(nr.as<u32>() + (size_t)sl * 2 * ell * CT, c->rgsw_pool.as<u32>() + (size_t)sl * 2 * ell * CT,
-                           2 * ell * CT * 4, cudaMemcpyDeviceToDevice, c->stream));
-    }
-    CK(cudaStreamSynchronize(c->stream));
-    c->evk_pool.release();
-    c->rgsw_pool.release();
-    c->evk_pool = ne;
-    c->rgsw_pool = nr;
-    ne.p = nullptr;
-    nr.p = nullptr;
-    c->slot_stages.resize(ns, -1);
-    c->slot_rgsw.resize(ns, 0);
-    c->key_slots = ns;
-    c->key_stages = want_stages;
-  }
-  DevBuf tmp;
   const size_t ew = (size_t)stages * ell * CT, rw = 2 * ell * CT;
-  if ((rc = tmp.ensure(std::max(ew, rw) * 4))) return rc;
+  DevBuf tmp, brv;
+  if ((rc = tmp.ensure(std::max<size_t>(ew + rw, 1) * 4)) || (rc = brv.ensure(std::max<size_t>(ew + rw, 1) * 4)))
+    return rc;
   if (stages) {
     CK(cudaMemcpyAsync(tmp.p, evks, ew * 4, cudaMemcpyHostToDevice, c->stream));
-    u32* dst = c->evk_pool.as<u32>() + (size_t)slot * c->key_stages * ell * CT;
-    if ((rc = bitrev_rows(c, tmp.as<u32>(), dst, ew >> c->logn, c->stream))) return rc;
-    if ((rc = fold_rows(c, dst, dst, 1, (int)stages, 0, ell * CT, 0, ell * CT, c->stream))) return rc;
-    CK(cudaStreamSynchronize(c->stream));
+    if ((rc = bitrev_rows(c, tmp.as<u32>(), brv.as<u32>(), ew >> c->logn, c->stream))) return rc;
   }
-  c->slot_rgsw[slot] = 0;
   if (sk_rgsw) {
-    CK(cudaMemcpyAsync(tmp.p, sk_rgsw, rw * 4, cudaMemcpyHostToDevice, c->stream));
-    u32* dst = c->rgsw_pool.as<u32>() + (size_t)slot * rw;
-    if ((rc = bitrev_rows(c, tmp.as<u32>(), dst, rw >> c->logn, c->stream))) return rc;
-    if ((rc = fold_rows(c, dst, dst, 1, 2, 0, ell * CT, 0, ell * CT, c->stream))) return rc;
-    CK(cudaStreamSynchronize(c->stream));
-    c->slot_rgsw[slot] = 1;
+    CK(cudaMemcpyAsync(tmp.as<u32>() + ew, sk_rgsw, rw * 4, cudaMemcpyHostToDevice, c->stream));
+    if ((rc = bitrev_rows(c, tmp.as<u32>() + ew, brv.as<u32>() + ew, rw >> c->logn, c->stream))) return rc;
   }
-  c->slot_stages[slot] = (int)stages;
+  rc = install_keys_brv(c, slot, brv.as<u32>(), stages, sk_rgsw ? brv.as<u32>() + ew : nullptr);
   tmp.release();
-  return 0;
+  brv.release();
+  return rc;
+}
+
+#define DISPATCH_CASE_CKG(L, K_, E) \
+  case L * 10000 + K_ * 100 + E:    \
+    return Engine<L, K_, E>::client_keygen(c, slot, stages, seed, secret_out);
+
+int gpir_client_keygen(gpir_ctx* c, int slot, uint32_t stages, uint64_t seed, uint32_t error_bound,
+                       int8_t* secret_out) {
+  if (!c || slot < 0 || stages > 31) FAIL(GPIR_INVALID_ARGUMENT, "invalid client keygen request");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  c->error_bound = error_bound;
+  switch (c->logn * 10000 + c->k * 100 + c->ell) {
+    GPIR_COMBOS(DISPATCH_CASE_CKG)
+    default:
+      FAIL(GPIR_UNSUPPORTED, "unsupported combination");
+  }
+}
+
+#define DISPATCH_CASE_CQ(L, K_, E) \
+  case L * 10000 + K_ * 100 + E:   \
+    return Engine<L, K_, E>::client_queries(c, secret, plain_bits, d0, d1, i_star, j_star, count, seed, queries_out);
+
+int gpir_client_queries(gpir_ctx* c, const int8_t* secret, uint32_t plain_bits, uint32_t error_bound, uint32_t d0,
+                        uint32_t d1, const uint32_t* i_star, const uint32_t* j_star, uint32_t count, uint64_t seed,
+                        uint32_t* queries_out) {
+  if (!c || !secret || !i_star || !j_star || !queries_out || !d0 || !d1 || (d1 & (d1 - 1)))
+    FAIL(GPIR_INVALID_ARGUMENT, "invalid client query request");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  c->error_bound = error_bound;
+  if (!count) return 0;
+  switch (c->logn * 10000 + c->k * 100 + c->ell) {
+    GPIR_COMBOS(DISPATCH_CASE_CQ)
+    default:
+      FAIL(GPIR_UNSUPPORTED, "unsupported combination");
+  }
 }
 
 int gpir_keys_drop(gpir_ctx* c, int slot) {
