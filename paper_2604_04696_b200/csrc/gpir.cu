@@ -356,6 +356,8 @@ struct Engine {
     const int sm = (int)fused_smem();
     CK(cudaFuncSetAttribute(k_eq_fused<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_xp_fused<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute(k_eq_nttmac<LOGN, K, ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)k2eq_dyn_smem<LOGN>()));
     done = true;
     return 0;
   }
@@ -388,7 +390,7 @@ struct Engine {
         const int nn = (int)std::min(cn, nodes - n0);
         k_eq_dcp<LOGN, K, ELL><<<nn, T, 0, s>>>(state, (int)n0, k_aut, c->ws_dig.as<int>(), c->tb, c->cc, c->tc);
         CKL();
-        k_eq_nttmac<LOGN, K, ELL><<<nn * K, T, 0, s>>>(
+        k_eq_nttmac<LOGN, K, ELL><<<nn * K, T, k2eq_dyn_smem<LOGN>(), s>>>(
             state, C, (int)n0, c->ws_dig.as<int>(), ksk, k_aut, mono, out, Cout, c->tb, c->tc);
         CKL();
         *launches += 2;
@@ -414,7 +416,7 @@ struct Engine {
       CKL();
       if (g_sprof.fine) g_sprof.mark(s, "  eq_dcp");
       if (mode == 3) {  // hybrid: the digit NTTs stream straight into the key-switch MAC (K2)
-        k_eq_nttmac<LOGN, K, ELL><<<nn * K, T, 0, s>>>(state, C, (int)n0, c->ws_dig.as<int>(), ksk, k_aut, mono,
+        k_eq_nttmac<LOGN, K, ELL><<<nn * K, T, k2eq_dyn_smem<LOGN>(), s>>>(state, C, (int)n0, c->ws_dig.as<int>(), ksk, k_aut, mono,
                                                        out, Cout, c->tb, c->tc);
         CKL();
         *launches += 3;

@@ -111,8 +111,16 @@ __device__ __forceinline__ u32 mod_add(u32 a, u32 b, u32 q) { return csub(a + b,
 // 32-bit x and y < q.  Four IMAD-class ops and a 32-bit accumulator (no
 // 64-bit register pairs); `terms` such products stay in int32 while
 // terms * q < 2^31.
+#ifndef MONT_WIDE
+#define MONT_WIDE 1
+#endif
 __device__ __forceinline__ void mont_mac(int& acc, u32 x, u32 y, u32 q, u32 qinv) {
+#if MONT_WIDE  // one IMAD.WIDE (quarter rate) for both halves instead of IMAD + IMAD.HI
+  const u64 p = (u64)x * y;
+  const u32 lo = (u32)p, hi = (u32)(p >> 32);
+#else
   const u32 lo = x * y, hi = __umulhi(x, y);
+#endif
   acc += (int)(hi - __umulhi(lo * qinv, q));
 }
 

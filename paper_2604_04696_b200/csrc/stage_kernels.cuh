@@ -170,7 +170,17 @@ __device__ __forceinline__ void k2_mac(NttState& ns, const int* __restrict__ dig
 #define K2_MINB 3
 #endif
 
-// K2, ExpandQuery: node (node0 + blockIdx.x / K), output limb blockIdx.x % K
+// K2, ExpandQuery: node (node0 + blockIdx.x / K), output limb blockIdx.x % K.
+// The node's input limb i (a and b components, 2 x 16 KiB) is bulk-copied into
+// dynamic shared memory at kernel start (one cp.async.bulk pair, mbarrier) and
+// lands while the digit transforms run, so the epilogue's automorphism gathers
+// (direct term and combine) read shared memory (<= 2-way bank conflicts for
+// the stages run here) instead of issuing scattered 4-byte L2 loads.
+template <int LOGN>
+constexpr size_t k2eq_dyn_smem() {
+  return 2 * ((size_t)4 << LOGN) + 16;
+}
+
 template <int LOGN, int K, int ELL>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T, K2_MINB)
     k_eq_nttmac(const u32* __restrict__ state, int C, int node0, const int* __restrict__ dig, RowsDesc ksk, u32 k_aut,
@@ -184,35 +194,45 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, K2_MINB)
   const int gn = node0 + ln;
   const int b = gn / C, c = gn % C;
   const size_t CT = 2 * (size_t)K * N;
+  const u32* st = state + (size_t)gn * CT;
+  extern __shared__ __align__(128) u32 k2_in[];  // [a limb i | b limb i]
+  uint64_t* inbar = reinterpret_cast<uint64_t*>(k2_in + 2 * N);
+  if (tid == 0) {
+    mbar_init(inbar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(inbar, 2u * N * 4u);
+    bulk_g2s(k2_in, st + (size_t)i * N, N * 4u, inbar);
+    bulk_g2s(k2_in + N, st + (size_t)(K + i) * N, N * 4u, inbar);
+  }
+  const u32* in_a = k2_in;
+  const u32* in_b = k2_in + N;
   int acc0[16], acc1[16];
-  const u32* sta = state + (size_t)gn * CT + (size_t)i * N;
   k2_mac<LOGN, K, ELL>(
       ns, dig + (size_t)ln * ELL * N, 1, i, [&](int j) { return ksk.row(b, j, ELL, CT); },
       [&](int, int h, u32(&x)[4]) {
+        if (h == 0) mbar_wait(inbar, 0);  // the transforms' barriers order the init before every wait
 #pragma unroll
-        for (int r = 0; r < 4; ++r) x[r] = __ldg(sta + aut_src((tid << 4) + 4 * h + r, k_aut, LOGN));
+        for (int r = 0; r < 4; ++r) x[r] = in_a[aut_src((tid << 4) + 4 * h + r, k_aut, LOGN)];
       },
       tb, tc, acc0, acc1);
   // combine (src/planner.py:361-363): out[c] = state + s, out[c + C] = X^-2^t (state - s)
   const Modulus M = tb.mod[i];
   const u32 q = M.q;
   const int i0 = tid << 4;
-  const u32* st = state + (size_t)gn * CT;
-  const u32* stb = st + (size_t)(K + i) * N;
   u32* o0 = out + ((size_t)b * Cout + c) * CT;
   u32* o1 = out + ((size_t)b * Cout + c + C) * CT;
   const bool second = c + C < Cout;
 #pragma unroll
   for (int h = 0; h < 4; ++h) {  // four quarters of 4 slots: few live registers
-    const uint4 ca = __ldg(reinterpret_cast<const uint4*>(st + (size_t)i * N + i0) + h);
-    const uint4 cb = __ldg(reinterpret_cast<const uint4*>(stb + i0) + h);
+    const uint4 ca = reinterpret_cast<const uint4*>(in_a + i0)[h];
+    const uint4 cb = reinterpret_cast<const uint4*>(in_b + i0)[h];
     const u32 cav[4] = {ca.x, ca.y, ca.z, ca.w}, cbv[4] = {cb.x, cb.y, cb.z, cb.w};
     u32 xa[4], xb[4], ya[4], yb[4];
 #pragma unroll
     for (int rr = 0; rr < 4; ++rr) {
       const int r = 4 * h + rr;
       const u32 sa = mont_fin(acc0[r], ELL, M);
-      const u32 sb = mod_add(mont_fin(acc1[r], ELL, M), __ldg(stb + aut_src(i0 + r, k_aut, LOGN)), q);
+      const u32 sb = mod_add(mont_fin(acc1[r], ELL, M), in_b[aut_src(i0 + r, k_aut, LOGN)], q);
       xa[rr] = mod_add(cav[rr], sa, q);
       xb[rr] = mod_add(cbv[rr], sb, q);
       const uint2 w = __ldg(&mono[(size_t)i * N + i0 + r]);
