@@ -526,11 +526,27 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
   const int nd = blockIdx.x, i = blockIdx.y;
   const u32* row = state + ((size_t)(node0 + nd) * 2 * K + i) * N;
   u32* dst = coeff + ((size_t)nd * K + i) * N;
+  // the row arrives by one bulk copy into the exchange buffer the transform
+  // does not use; the automorphism gather then reads shared memory
+  __shared__ uint64_t bar;
+  u32* stage = xbuf + N;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, N * 4u);
+    bulk_g2s(stage, row, N * 4u, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
   ntt_inv<LOGN>(
       ns, tb.inv + (size_t)i * N, tc.i[i], tb.mod[i],
       [&](int i0, u32(&x)[16]) {
 #pragma unroll
+#ifndef EQ_INTT_GLOBAL
+        for (int r = 0; r < 16; ++r) x[r] = stage[aut_src(i0 + r, k_aut, LOGN)];
+#else
         for (int r = 0; r < 16; ++r) x[r] = __ldg(row + aut_src(i0 + r, k_aut, LOGN));
+#endif
       },
       [&](int j, int, u32 v) { dst[j] = v; });
 }
