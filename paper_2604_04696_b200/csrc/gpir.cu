@@ -505,6 +505,35 @@ struct Engine {
     return db->d0 <= 1024 && KN % PK_P == 0;
   }
 
+  // byte-plane packing of R rows x Kd into the canonical tiles (k_pack_planes2
+  // with 32 p per CTA; GPIR_PACK=16: 16 p, GPIR_PACK=1: the p-blocked k_pack_planes)
+  static int pack_planes(const PackSrc& src, int R, int Kd, int RT, int ntiles, int nchunks, int kc, uint8_t* dst,
+                         int KN, cudaStream_t s) {
+    static const bool old_pack = getenv("GPIR_PACK") && atoi(getenv("GPIR_PACK")) == 1;
+    if (old_pack) {
+      dim3 g(KN / PK_P, (ntiles * RT + PK_R - 1) / PK_R, nchunks * (kc / PK_K));
+      k_pack_planes<<<g, 256, 0, s>>>(src, R, Kd, RT, ntiles, nchunks, kc, dst);
+      CKL();
+      return 0;
+    }
+    static const int pw = getenv("GPIR_PACK") && atoi(getenv("GPIR_PACK")) == 16 ? 16 : 32;
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_pack_planes2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, Pk2<16>::SMEM));
+      CK(cudaFuncSetAttribute(k_pack_planes2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, Pk2<32>::SMEM));
+      attr = true;
+    }
+    if (pw == 16) {
+      dim3 g(KN / 16, (ntiles * RT + Pk2<16>::RR - 1) / Pk2<16>::RR, nchunks * (kc / PK_K));
+      k_pack_planes2<16><<<g, 256, Pk2<16>::SMEM, s>>>(src, R, Kd, RT, ntiles, nchunks, kc, dst);
+    } else {
+      dim3 g(KN / 32, (ntiles * RT + Pk2<32>::RR - 1) / Pk2<32>::RR, nchunks * (kc / PK_K));
+      k_pack_planes2<32><<<g, 256, Pk2<32>::SMEM, s>>>(src, R, Kd, RT, ntiles, nchunks, kc, dst);
+    }
+    CKL();
+    return 0;
+  }
+
   // RowSel: tensor-core path (byte-plane u8 GEMMs, rowsel_tc.cuh) when the
   // shape allows, else the CUDA-core kernel.  ev_mid (if non-null) is
   // recorded between operand packing and the GEMM.
@@ -538,17 +567,15 @@ struct Engine {
         if ((rc = db->d8.ensure((size_t)KN * nchunks * ntiles * 4 * NT * KC))) return rc;
         CK(cudaMemsetAsync(db->d8.p, 0, db->d8.bytes, s));
         PackSrc ps{db->data.as<u32>(), (size_t)db->d0 * KN, 0, 1, (size_t)KN};
-        dim3 g(KN / PK_P, (ntiles * NT + PK_R - 1) / PK_R, nchunks * (KC / PK_K));
-        k_pack_planes<<<g, 256, 0, s>>>(ps, (int)db->d1, (int)db->d0, NT, ntiles, nchunks, KC, db->d8.as<uint8_t>());
+        if ((rc = pack_planes(ps, (int)db->d1, (int)db->d0, NT, ntiles, nchunks, KC, db->d8.as<uint8_t>(), KN, s)))
+          return rc;
         CKL();
         db->d8_nt = NT;
         db->d8_kc = KC;
       }
       if ((rc = c->ws_a8.ensure((size_t)KN * nchunks * mtiles * 4 * RA * KC))) return rc;
       PackSrc pa{leaves, a_b_words, (size_t)KN, 2, 2 * (size_t)KN};
-      dim3 g(KN / PK_P, (mtiles * RA + PK_R - 1) / PK_R, nchunks * (KC / PK_K));
-      k_pack_planes<<<g, 256, 0, s>>>(pa, M, (int)db->d0, RA, mtiles, nchunks, KC, c->ws_a8.as<uint8_t>());
-      CKL();
+      if ((rc = pack_planes(pa, M, (int)db->d0, RA, mtiles, nchunks, KC, c->ws_a8.as<uint8_t>(), KN, s))) return rc;
       if (ev_mid) CK(cudaEventRecord(ev_mid, s));
       TcArgs ta;
       ta.A8 = c->ws_a8.as<uint8_t>();

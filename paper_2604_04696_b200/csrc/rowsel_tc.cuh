@@ -175,6 +175,77 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Row-blocked packer: one CTA covers P p x (1024 / P) rows x one 16-byte K
+// group, so every warp store is 32 consecutive rows of one (p, plane) -- 512
+// contiguous bytes of the canonical layout (k_pack_planes writes 16-byte
+// pieces, one per p) -- while the reads are runs of P p (4P bytes).  The shared
+// tile is [k][p][row] with a padded p stride RS: conflict-free for the
+// row-per-lane reads and for the (row, 4 p) stores of the load phase.
+template <int P>
+struct Pk2 {
+  static constexpr int RR = 1024 / P;                // rows per CTA
+  static constexpr int RS = P == 16 ? 66 : 33;       // padded p stride (words)
+  static constexpr int SMEM = PK_K * P * RS * 4;
+};
+template <int P>
+__global__ void __launch_bounds__(256)
+    k_pack_planes2(PackSrc src, int R, int Kd, int RT, int ntiles, int nchunks, int kc, uint8_t* __restrict__ dst) {
+  using C = Pk2<P>;
+  extern __shared__ __align__(16) u32 pk2[];  // [k 16][p P][RS]
+  const int p0 = blockIdx.x * P;
+  const int r0 = blockIdx.y * C::RR;
+  const int kg = blockIdx.z;
+  const int c = kg / (kc / PK_K), g = kg % (kc / PK_K);
+  const int tid = threadIdx.x;
+  {  // load: thread -> row r0 + tid / (P / 4), p quarter tid % (P / 4), all 16 k
+    const int row = tid / (P / 4), q4 = tid % (P / 4);
+    const int r = r0 + row;
+    const size_t roff = r < R ? pack_src_off(src, r) : 0;
+    uint4 v[PK_K];
+#pragma unroll
+    for (int k = 0; k < PK_K; ++k) {
+      const int kk = kg * PK_K + k;
+      v[k] = (r < R && kk < Kd)
+                 ? __ldg(reinterpret_cast<const uint4*>(src.base + roff + (size_t)kk * src.k_stride + p0) + q4)
+                 : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < PK_K; ++k) {
+      u32* t = pk2 + (k * P + 4 * q4) * C::RS + row;
+      t[0] = v[k].x;
+      t[C::RS] = v[k].y;
+      t[2 * C::RS] = v[k].z;
+      t[3 * C::RS] = v[k].w;
+    }
+  }
+  __syncthreads();
+  const int rpad = ((R + RT - 1) / RT) * RT;
+  const int row = tid % C::RR;
+  const int r = r0 + row;
+  if (r >= rpad) return;
+  const int nt = r / RT, rin = r % RT;
+#pragma unroll
+  for (int i = 0; i < P * C::RR / 256; ++i) {
+    const int pp = tid / C::RR + (256 / C::RR) * i;
+    u32 w[4][4];  // [plane][word]
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      u32 x[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) x[b] = pk2[((q4 * 4 + b) * P + pp) * C::RS + row];
+#pragma unroll
+      for (int pl = 0; pl < 4; ++pl)
+        w[pl][q4] = __byte_perm(__byte_perm(x[0], x[1], pl | ((pl + 4) << 4)),
+                                __byte_perm(x[2], x[3], pl | ((pl + 4) << 4)), 0x5410);
+    }
+    const size_t blk = (((size_t)(p0 + pp) * nchunks + c) * ntiles + nt) * (size_t)(4 * RT * kc);
+#pragma unroll
+    for (int pl = 0; pl < 4; ++pl)
+      *reinterpret_cast<uint4*>(dst + blk + (size_t)pl * RT * kc + ((size_t)g * RT + rin) * 16) =
+          make_uint4(w[pl][0], w[pl][1], w[pl][2], w[pl][3]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the tensor-core GEMM
 struct TcArgs {
