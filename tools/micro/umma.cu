@@ -11,20 +11,29 @@
 
 using namespace gpir;
 
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
 
 // ST > 0: warps 1-4 write TMEM (tcgen05.st); ST < 0: warps 1-8 read TMEM (tcgen05.ld, the epilogue pattern);
 // ST >= 100: warps 1-8 stream shared memory (ld.shared.v4 + st.shared.v4 of a private 2 KiB block each);
 // ST == 60 / 61: one / two warps stream bulk copies (16 KiB, 2-stage rings) into shared memory meanwhile;
 // ST == 50 / 51: one / two tcgen05.commit (to mbarriers nobody waits on) after every 16 MMAs
-template <int M, int N, bool TA, bool CP, int ST = 0>
+template <int M, int N, bool TA, bool CP, int ST = 0, bool RND = false>
 __global__ void __launch_bounds__(288, 1) k_umma(int iters, unsigned long long* out, const uint8_t* src) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar, dummy[2];
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5;
   // operands: A 4 planes x M x 32 B, B 4 planes x N x 32 B (zeros: data-oblivious)
-  for (int i = threadIdx.x; i < (4 * M * 32 + 4 * N * 32) / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < (4 * M * 32 + 4 * N * 32) / 16; i += blockDim.x) {
+    // RND: random operand bytes (the tensor pipe's rate may depend on the data through power)
+    const uint32_t h = RND ? (uint32_t)(i * 2654435761u) ^ (uint32_t)(blockIdx.x * 40503u) : 0u;
+    reinterpret_cast<uint4*>(sm)[i] = make_uint4(h, h * 747796405u + 1u, h ^ 0x9E3779B9u, h * 2891336453u + 7u);
+  }
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_init(&dummy[0], 1);
@@ -146,14 +155,14 @@ __global__ void __launch_bounds__(288, 1) k_umma(int iters, unsigned long long* 
 }
 
 static const uint8_t* g_src = nullptr;
-template <int M, int N, bool TA, bool CP, int ST = 0>
+template <int M, int N, bool TA, bool CP, int ST = 0, bool RND = false>
 void run(const char* name, unsigned long long* d, int sms) {
   const int iters = 2000;
   const int smem = 4 * M * 32 + 4 * N * 32 + 1024 + 2 * 32768;
-  cudaFuncSetAttribute(k_umma<M, N, TA, CP, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_umma<M, N, TA, CP, ST, RND>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (int rep = 0; rep < 2; ++rep) {
     cudaMemset(d, 0, 8);
-    k_umma<M, N, TA, CP, ST><<<sms, 288, smem>>>(iters, d, g_src);
+    k_umma<M, N, TA, CP, ST, RND><<<sms, 288, smem>>>(iters, d, g_src);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       printf("%s: %s\n", name, cudaGetErrorString(e));
@@ -198,6 +207,9 @@ int main() {
   run<128, 32, true, false, 60>("M128 N32 TS + TMA(1 warp)", d, sms);
   run<128, 32, true, false, 61>("M128 N32 TS + TMA(2 warps)", d, sms);
   run<64, 64, false, false, 61>("M64 N64 SS + TMA(2 warps)", d, sms);
+  run<128, 32, true, false, 0, true>("M128 N32 TS random data", d, sms);
+  run<128, 32, true, true, 0, true>("M128 N32 TS + cp random", d, sms);
+  run<64, 64, false, false, 0, true>("M64 N64 SS random data", d, sms);
   run<128, 32, true, false, 101>("M128 N32 TS + smem(1)", d, sms);
   run<128, 32, true, false, 104>("M128 N32 TS + smem(4)", d, sms);
   run<128, 32, true, true, 101>("M128 N32 TS + cp + smem(1)", d, sms);
