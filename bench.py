@@ -341,6 +341,8 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": desc, "d0": d0, "d1": d1, "global_batch": B * world, "per_gpu_batch": B,
                    "record_bytes": rb, "plain_bits": pb, "encoded_db_bytes": d0 * d1 * KN * 4,
                    "l2": f"inputs larger than L2 ({d0 * d1 * KN * 4 >> 30} GiB DB streamed by RowSel every step)",
+                   "cuda_graph": "timed steps replay the pipeline as a CUDA graph (library default, recorded during "
+                                 "warm-up); phases_ms come from eager passes with per-phase events",
                    "parallelism": "replica" if world > 1 else "single",
                    "plan_eq": "".join("oFSH"[v] for v in em[:stages]),
                    "plan_ct": "".join("oFSH"[v] for v in cm[:max(d1.bit_length() - 1, 0)]),

@@ -93,6 +93,13 @@ int gpir_ctx_device(const gpir_ctx* ctx);
 /* RowSel engine: 0 = auto (tensor cores when d0 <= 1024; A tiles of 128 rows),
  * 1 = CUDA cores (64-bit lazy IMAD), 2 = tensor cores (tcgen05 kind::i8). */
 int gpir_set_rowsel_engine(gpir_ctx* ctx, int engine);
+
+/* CUDA-graph replay of the device pipeline (default on; GPIR_GRAPH=0 in the
+ * environment turns it off for new contexts).  Calls without stats and without
+ * stage timing record the pipeline of a (db, B, buffers, plan) shape on its
+ * second call and replay the graph from the third; any device (re)allocation
+ * invalidates the recorded graphs. */
+int gpir_set_graphs(gpir_ctx* ctx, int on);
 /* Supported (log2 n, k, ell) combinations are compiled in; 1 if supported. */
 int gpir_supported(uint32_t n, uint32_t k, uint32_t ell);
 

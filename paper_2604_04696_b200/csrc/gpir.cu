@@ -9,7 +9,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -56,11 +58,16 @@ typedef unsigned __int128 u128;
 // ---------------------------------------------------------------------------
 // device buffer helper
 
+// bumped by every (re)allocation of a device buffer: captured CUDA graphs
+// hold raw pointers, so a graph is only replayed while this is unchanged
+static std::atomic<uint64_t> g_alloc_gen{0};
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   int ensure(size_t want) {
     if (want <= bytes) return 0;
+    ++g_alloc_gen;
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -75,7 +82,10 @@ struct DevBuf {
     return 0;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaFree(p);
+      ++g_alloc_gen;
+    }
     p = nullptr;
     bytes = 0;
   }
@@ -119,6 +129,21 @@ struct gpir_ctx {
   uint32_t sh_B = 0, sh_d0 = 0, sh_d1 = 0, sh_total = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[12];
+  // CUDA graphs of the device pipeline (answer_dev), keyed by everything the
+  // captured launches bake in; the first call of a key runs eagerly (lazy
+  // allocations, DB byte-plane packing), the second captures, later ones replay
+  struct GraphEntry {
+    const void* db = nullptr;
+    const void* dq = nullptr;
+    const void* dout = nullptr;
+    int B = 0;
+    uint64_t gen = 0;
+    std::vector<uint8_t> modes;
+    int state = 0;  // 1 seen once, 2 captured, -1 capture failed (stay eager)
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<GraphEntry> graphs;
+  int use_graph = 1;  // GPIR_GRAPH=0 disables
   std::mutex mu;
   size_t ct_words() const { return 2 * (size_t)k * n; }
 };
@@ -615,7 +640,18 @@ struct Engine {
                                   : (PST == 2   ? k_rowsel_tc<32, false, 2, 32>
                                      : PST == 4 ? k_rowsel_tc<32, false, 4, 32>
                                                 : k_rowsel_tc<32, false, 8, 32>));
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      {  // the attribute is set once per (device, kernel, size): no API calls inside a graph capture
+        static std::mutex mu;
+        static std::vector<std::tuple<int, const void*, size_t>> smem_set;
+        std::lock_guard<std::mutex> lk(mu);
+        bool have = false;
+        for (auto& ks : smem_set)
+          have |= (std::get<0>(ks) == c->device && std::get<1>(ks) == (const void*)kern && std::get<2>(ks) >= smem);
+        if (!have) {
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          smem_set.emplace_back(c->device, (const void*)kern, smem);
+        }
+      }
       kern<<<grid, TC_THREADS, smem, s>>>(ta, c->tb);
       CKL();
       if (prof_on) {
@@ -799,12 +835,58 @@ struct Engine {
     if ((rc = ensure_ws(c, B, total, d1, bits))) return rc;
     if (st) CK(cudaEventRecord(c->ev[0], s));
     CK(cudaMemcpyAsync(c->ws_kslot.p, slots, (size_t)B * 4, cudaMemcpyHostToDevice, s));
-    if ((rc = bitrev_rows(c, d_q, c->ws_state0.as<u32>(), (size_t)B * 2 * K, s))) return rc;
-    u32* res = nullptr;
-    if (st) st->launches += 2;
-    if ((rc = pipeline(c, db, d1, B, eq_modes, n_eq, ct_modes, n_ct, c->ws_kslot.as<int>(), s, st, &res, nullptr)))
-      return rc;
-    if ((rc = bitrev_rows(c, res, d_out, (size_t)B * 2 * K, s))) return rc;
+    auto body = [&]() -> int {
+      int r;
+      if ((r = bitrev_rows(c, d_q, c->ws_state0.as<u32>(), (size_t)B * 2 * K, s))) return r;
+      u32* res = nullptr;
+      if (st) st->launches += 2;
+      if ((r = pipeline(c, db, d1, B, eq_modes, n_eq, ct_modes, n_ct, c->ws_kslot.as<int>(), s, st, &res, nullptr)))
+        return r;
+      return bitrev_rows(c, res, d_out, (size_t)B * 2 * K, s);
+    };
+    // graph replay: not with per-phase stats or stage timing (their events and syncs)
+    if (c->use_graph && !st && !c->stage_timing && !g_sprof.env) {
+      std::vector<uint8_t> modes(34, 0);
+      modes[0] = (uint8_t)n_eq;
+      modes[1] = (uint8_t)n_ct;
+      for (uint32_t j = 0; j < n_eq && j < 16 && eq_modes; ++j) modes[2 + j] = eq_modes[j];
+      for (uint32_t j = 0; j < n_ct && j < 16 && ct_modes; ++j) modes[18 + j] = ct_modes[j];
+      const uint64_t gen = g_alloc_gen.load();
+      gpir_ctx::GraphEntry* e = nullptr;
+      for (auto& g : c->graphs)
+        if (g.db == db && g.dq == d_q && g.dout == d_out && g.B == B && g.gen == gen && g.modes == modes) e = &g;
+      if (!e) {
+        if (c->graphs.size() >= 16) {
+          if (c->graphs.front().exec) cudaGraphExecDestroy(c->graphs.front().exec);
+          c->graphs.erase(c->graphs.begin());
+        }
+        gpir_ctx::GraphEntry ne;
+        ne.db = db, ne.dq = d_q, ne.dout = d_out, ne.B = B, ne.gen = gen, ne.modes = modes, ne.state = 1;
+        c->graphs.push_back(ne);
+        return body();  // first call eager
+      }
+      if (e->state == 2) {
+        CK(cudaGraphLaunch(e->exec, s));
+        return 0;
+      }
+      if (e->state == 1) {  // capture, instantiate, launch; on any failure stay eager for this key
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const int r = body();
+        const cudaError_t ce = cudaStreamEndCapture(s, &g);
+        if (!r && ce == cudaSuccess && g && cudaGraphInstantiate(&e->exec, g, 0) == cudaSuccess) {
+          cudaGraphDestroy(g);
+          e->state = 2;
+          CK(cudaGraphLaunch(e->exec, s));
+          return 0;
+        }
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        e->state = -1;
+        e->exec = nullptr;
+      }
+    }
+    if ((rc = body())) return rc;
     if (st) {
       CK(cudaEventRecord(c->ev[6], s));
       CK(cudaEventSynchronize(c->ev[6]));
@@ -1314,6 +1396,7 @@ gpir_ctx* gpir_ctx_create(int device, uint32_t n, uint32_t k, const uint32_t* q,
     return nullptr;
   }
   cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (const char* ge = getenv("GPIR_GRAPH")) c->use_graph = atoi(ge);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   for (auto& ev : c->ev) cudaEventCreate(&ev);
   return c;
@@ -1328,11 +1411,20 @@ void gpir_ctx_destroy(gpir_ctx* c) {
                     &c->ws_dn, &c->ws_io0, &c->ws_io1, &c->ws_a8})
     b->release();
   for (auto& ev : c->ev) cudaEventDestroy(ev);
+  for (auto& g : c->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   cudaStreamDestroy(c->stream);
   delete c;
 }
 
 int gpir_ctx_device(const gpir_ctx* c) { return c ? c->device : -1; }
+
+int gpir_set_graphs(gpir_ctx* c, int on) {
+  if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->use_graph = on ? 1 : 0;
+  return 0;
+}
 
 int gpir_set_rowsel_engine(gpir_ctx* c, int engine) {
   if (!c || engine < 0 || engine > 2) FAIL(GPIR_INVALID_ARGUMENT, "engine must be 0 (auto), 1 (CUDA cores) or 2 (tensor cores)");

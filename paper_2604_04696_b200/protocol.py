@@ -381,11 +381,13 @@ def answer_raw(qarr: np.ndarray, client_ids, keys_by_client, db, params, hw: Har
     if out is None:
         out = np.empty_like(qarr)
     nat.check(ctx.lib.gpir_set_rowsel_engine(ctx.h, _ENGINES[engine]), "rowsel engine")
-    st = nat.GpirStats()
+    # per-phase events only when asked for: without them the library replays a
+    # captured CUDA graph of the pipeline from the third call of a shape on
+    st = nat.GpirStats() if stats is not None else None
     t0 = time.perf_counter()
     nat.check(ctx.lib.gpir_answer_batch(ctx.h, ddb.handle, nat.ptr(qarr), nat.ptr(slots, nat.C.c_int32), B,
                                         nat.ptr(em, nat.C.c_uint8), len(em), nat.ptr(cm, nat.C.c_uint8), len(cm),
-                                        nat.ptr(out), nat.C.byref(st)), "answer_batch")
+                                        nat.ptr(out), nat.C.byref(st) if st is not None else None), "answer_batch")
     wall = time.perf_counter() - t0
     if stats is not None:
         stats.add_phase(Phase.EXPAND_QUERY.value, st.ms_expand / 1e3)

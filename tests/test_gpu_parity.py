@@ -280,3 +280,32 @@ def test_full_size_decrypt_property(G):
     for (c, i, j), r in zip(targets, resp):
         m = O.decrypt(clients[c], r.ct.raw())
         assert O.decode_plain(m, rb, po) == buf[i * d1 + j].tobytes()
+
+
+@pytest.mark.parametrize("name", ["prod_4x4", "proto_8x8"])
+def test_graph_replay_matches_eager(G, golden, name):
+    """Calls without per-phase stats record the pipeline as a CUDA graph on the
+    second call of a shape and replay it from the third: with new query contents
+    every replay must equal the eager path (stats requested), and the first
+    batch must still decrypt to its records."""
+    from paper_2604_04696_b200 import protocol
+    cases, _ = golden
+    case = cases[name]
+    po, records, clients, db, out0, resp = _run_case(G, case)
+    p = to_api(po)
+    keys = {cid: api_keys(p, c) for cid, c in clients.items()}
+    ids = [cid for cid, _, _ in case["queries"]]
+    q0 = np.stack([r.ct.raw() for r in resp])  # any valid (B, 2, k, n) input shape; contents vary below
+    qs = [api_query(p, q, cid, s) for s, (q, (cid, _, _)) in
+          enumerate(zip(rebuild_case(case)[3], case["queries"]))]
+    first = np.stack([q.ct.raw() for q in qs]).astype(np.uint32)
+    rng = np.random.default_rng(17)
+    qmod = np.array(po.ring.qs, dtype=np.uint64)[:, None]
+    batches = [first] + [(rng.integers(0, 1 << 62, size=q0.shape, dtype=np.uint64) % qmod).astype(np.uint32)
+                         for _ in range(4)] + [first]
+    for i, qa in enumerate(batches):
+        g = protocol.answer_raw(np.ascontiguousarray(qa), ids, keys, db, p)          # graph path (3rd call on)
+        e = protocol.answer_raw(np.ascontiguousarray(qa), ids, keys, db, p, stats=G.ServeStats())  # eager
+        assert np.array_equal(g, e), f"batch {i}: graph replay differs from the eager pipeline"
+        if i in (0, len(batches) - 1):
+            assert np.array_equal(g, out0)
