@@ -107,6 +107,38 @@ def ncu_traffic(prefix="k_rowsel_tc"):
     return best
 
 
+def dominant_kernel():
+    """The largest-share kernel of the newest committed ncu launch list (one config-2
+    bench step, profiles/*_ncu.json) with its pipe counters from the full capture:
+    the kernel `roofline` (RowSel, the north star's roofline target) is not."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu.json")), key=os.path.getmtime)
+    for f in reversed(files):
+        try:
+            js = json.load(open(f))
+        except Exception:
+            continue
+        ll = js.get("launch_list") or {}
+        if not ll:
+            continue
+        tot = sum(v["ns"] for v in ll.values())
+        name, v = max(ll.items(), key=lambda kv: kv[1]["ns"])
+        full = js.get("kernels", {}).get(name, {})
+
+        def pct(key):
+            m = full.get(key)
+            return float(m["value"]) / 100 if isinstance(m, dict) else None
+
+        return {"kernel": name, "share_of_launch_list": v["ns"] / tot,
+                "bound": "FMA-heavy integer pipe (IMAD, IMAD.HI)",
+                "fmaheavy_busy": pct("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                "issue_active": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                "phase_floor_frac": "see phase_roofline.ExpandQuery (live)",
+                "src": f"profiles/{os.path.basename(f)} (ncu launch list + --set full)"}
+    return None
+
+
 def phase_rooflines(d0, d1, B, k, n, ell, phases, rs_bytes, hbm_gbs, sms=148, clk_hz=1.965e9):
     """Per-phase roofline fractions.  The tree phases (ExpandQuery, RGSW
     assembly, ColTor) are bound by the FMA-heavy integer pipe: a Shoup
@@ -360,6 +392,7 @@ def run_ours(args, rank, world, local_rank):
                      "traffic": tr[0] if tr else None,
                      "traffic_src": f"profiles/{tr[1]} ({tr[2]}, ncu --set full)" if tr else None,
                      "algorithmic_bytes": rs_bytes, "avg_launch_ms": rs_ms},
+        "dominant_kernel": dominant_kernel(),
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu:
