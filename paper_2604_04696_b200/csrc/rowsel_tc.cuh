@@ -370,30 +370,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
         }
       }
     }
-  } else if (warp == 1) {  // MMA issuer: converged warp, one elected lane issues tcgen05.mma
+  } else if (warp == 1) {
+    // MMA issuer: one elected thread runs the whole schedule -- its mbarrier
+    // waits, fences and MMAs -- with no warp-wide convergence per stage, which
+    // would let the tensor pipe's shallow queue drain (tools/micro/umma_pipe.cu:
+    // 43 -> 33 cycles per M128 x N32 MMA with the per-stage tcgen05.cp)
     constexpr uint32_t idesc = umma_idesc_u8(M64 ? 64 : 128, TC_NT);
-    int s = 0;
-    uint32_t ph = 0;
-    int local = 0;
-    uint32_t ka = 0;                                        // A TMEM double-buffer index (TMEM_A)
-    const uint32_t a_ks = (2u * a.RA * 16u) >> 4;         // descriptor step of one 32-byte K step
-    const uint32_t a_pl = (uint32_t)(a.RA * TC_KC) >> 4;  // ... of one byte plane
-    for (Sched sc; sc.valid(a); sc.next(a), ++local) {
-      const int ab = (NBUF == 2) ? (local & 1) : 0;
-      const uint32_t aph = (NBUF == 2) ? ((local >> 1) & 1) : (local & 1);
-      long long t0 = clock64();
-      mbar_wait(&tempty[ab], aph ^ 1);
-      long long t1 = clock64();
-      if (a.prof && lane == 0) a.prof[blockIdx.x * 8 + 0] += t1 - t0;  // MMA waits for TMEM
-      tc_fence_after();
-      const uint32_t dcol = M64 ? tbase + ((uint32_t)(16 * ab) << 16) : tbase + ab * TC_ACC_COLS;
-      for (int c = 0; c < a.nchunks; ++c) {
-        long long t2 = clock64();
-        mbar_wait(&full[s], ph);
-        long long t3 = clock64();
-        if (a.prof && lane == 0) a.prof[blockIdx.x * 8 + 1] += t3 - t2;  // MMA waits for data
+    if (elect_one()) {
+      int s = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      uint32_t ka = 0;                                        // A TMEM double-buffer index (TMEM_A)
+      const uint32_t a_ks = (2u * a.RA * 16u) >> 4;         // descriptor step of one 32-byte K step
+      const uint32_t a_pl = (uint32_t)(a.RA * TC_KC) >> 4;  // ... of one byte plane
+      for (Sched sc; sc.valid(a); sc.next(a), ++local) {
+        const int ab = (NBUF == 2) ? (local & 1) : 0;
+        const uint32_t aph = (NBUF == 2) ? ((local >> 1) & 1) : (local & 1);
+        long long t0 = clock64();
+        mbar_wait(&tempty[ab], aph ^ 1);
+        long long t1 = clock64();
+        if (a.prof) a.prof[blockIdx.x * 8 + 0] += t1 - t0;  // MMA waits for TMEM
         tc_fence_after();
-        if (elect_one()) {
+        const uint32_t dcol = M64 ? tbase + ((uint32_t)(16 * ab) << 16) : tbase + ab * TC_ACC_COLS;
+        for (int c = 0; c < a.nchunks; ++c) {
+          long long t2 = clock64();
+          mbar_wait(&full[s], ph);
+          long long t3 = clock64();
+          if (a.prof) a.prof[blockIdx.x * 8 + 1] += t3 - t2;  // MMA waits for data
+          tc_fence_after();
           const uint32_t sa = smem_u32(stages + s * stage_bytes);
           const uint64_t a0 = umma_desc(sa, a.RA * 16, 128);
           const uint64_t b0 = umma_desc(sa + bytesA, TC_NT * 16, 128);
@@ -428,15 +432,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
           }
           umma_commit(&empty[s]);  // smem stage free once these MMAs retire
           if (c == a.nchunks - 1) umma_commit(&tfull[ab]);
-        }
-        __syncwarp();
-        if (a.prof && lane == 0) a.prof[blockIdx.x * 8 + 2] += clock64() - t3;  // MMA issue
-        if (++s == NS) {
-          s = 0;
-          ph ^= 1;
+          if (a.prof) a.prof[blockIdx.x * 8 + 2] += clock64() - t3;  // MMA issue
+          if (++s == NS) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
     }
+    __syncwarp();
   } else {  // epilogue warps 2..9: TMEM lanes 32*(warp%4) .. +31, column half (warp-2)/4
     constexpr int EPI_T = 32 * TC_EPI_WARPS;
     constexpr int HC = TC_NT / 2;  // columns per epilogue warp
