@@ -844,8 +844,11 @@ struct Engine {
         return r;
       return bitrev_rows(c, res, d_out, (size_t)B * 2 * K, s);
     };
-    // graph replay: not with per-phase stats or stage timing (their events and syncs)
-    if (c->use_graph && !st && !c->stage_timing && !g_sprof.env) {
+    // graph replay: not with per-phase stats or stage timing (their events and syncs), and
+    // not while the caller is itself capturing the stream (the launches then go into its graph)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(s, &cap));
+    if (c->use_graph && !st && !c->stage_timing && !g_sprof.env && cap == cudaStreamCaptureStatusNone) {
       std::vector<uint8_t> modes(34, 0);
       modes[0] = (uint8_t)n_eq;
       modes[1] = (uint8_t)n_ct;

@@ -309,3 +309,53 @@ def test_graph_replay_matches_eager(G, golden, name):
         assert np.array_equal(g, e), f"batch {i}: graph replay differs from the eager pipeline"
         if i in (0, len(batches) - 1):
             assert np.array_equal(g, out0)
+
+
+def test_caller_graph_capture(G, golden):
+    """A caller may record gpir_answer_batch_dev into its own CUDA graph (torch.cuda.CUDAGraph):
+    the library then launches eagerly into the caller's capture; replays equal the eager result."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2604_04696_b200 import _native as nat
+    from paper_2604_04696_b200 import protocol
+    cases, _ = golden
+    case = cases["prod_4x4"]
+    po, records, clients, db, out0, resp = _run_case(G, case)
+    p = to_api(po)
+    keys = {cid: api_keys(p, c) for cid, c in clients.items()}
+    ids = [cid for cid, _, _ in case["queries"]]
+    qs = [api_query(p, q, cid, s) for s, (q, (cid, _, _)) in
+          enumerate(zip(rebuild_case(case)[3], case["queries"]))]
+    qarr = np.stack([q.ct.raw() for q in qs]).astype(np.uint32)
+    protocol.answer_raw(qarr, ids, keys, db, p)  # keys into their slots
+    ddb = protocol._device_db(db, p)
+    ctx = ddb.ctx
+    stages = G.planner.num_expand_stages(G.planner.expansion_leaves(db.config.d0, db.config.d1, p.gadget.ell))
+    slots = torch.tensor([ctx.key_slot(keys[c], stages, db.config.d1 > 1) for c in ids], dtype=torch.int32).pin_memory()
+    d_q = torch.from_numpy(qarr.view(np.int32)).cuda()
+    d_o = torch.empty_like(d_q)
+    em = np.zeros(16, np.uint8)
+    cm = np.zeros(16, np.uint8)
+    nat.check(ctx.lib.gpir_plan(ctx.h, db.config.d0, db.config.d1, len(ids), nat.ptr(em, C.c_uint8), 16,
+                                nat.ptr(cm, C.c_uint8), 16), "plan")
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        def call():
+            nat.check(ctx.lib.gpir_answer_batch_dev(ctx.h, ddb.handle, C.c_void_p(d_q.data_ptr()),
+                                                    C.cast(C.c_void_p(slots.data_ptr()), C.POINTER(C.c_int32)),
+                                                    len(ids), nat.ptr(em, C.c_uint8), 16, nat.ptr(cm, C.c_uint8), 16,
+                                                    C.c_void_p(d_o.data_ptr()), C.c_void_p(s.cuda_stream), None),
+                      "answer_dev")
+        call()  # eager once (lazy allocations)
+        s.synchronize()
+        g.capture_begin()
+        call()
+        g.capture_end()
+    for _ in range(2):
+        d_o.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(d_o.cpu().numpy().view(np.uint32).reshape(out0.shape), out0)
