@@ -9,8 +9,8 @@
 #include "rowsel_tc.cuh"
 using namespace gpir;
 
-template <bool CP, bool PROD, bool ONE = false>
-__global__ void __launch_bounds__(64, 1) k(const uint8_t* src, int iters, int ns, unsigned long long* out) {
+template <bool CP, bool PROD, bool ONE = false, bool EPI = false>
+__global__ void __launch_bounds__(320, 1) k(const uint8_t* src, int iters, int ns, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   constexpr uint32_t BA = 16384, BD = 4096, SB = BA + BD;
   __shared__ uint64_t full[12], empty[12];
@@ -31,7 +31,26 @@ __global__ void __launch_bounds__(64, 1) k(const uint8_t* src, int iters, int ns
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tslot;
-  if (warp == 1) {  // producer
+  if (EPI && warp >= 2) {  // epilogue-like warps: TMEM loads of 7 diagonals + a shared-memory staging write
+    const uint32_t q = (uint32_t)(warp & 3) * 32;
+    u32* stg = reinterpret_cast<u32*>(sm + (size_t)ns * SB) + (warp - 2) * 32 * 33;
+    uint32_t acc = 0;
+    for (int it = 0; it < iters * 2; ++it) {
+      uint32_t v[7][8];
+#pragma unroll
+      for (int u = 0; u < 7; ++u) tmem_ld8(tbase + (q << 16) + u * 32 + 16 * ((warp - 2) >> 2), v[u]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        u64 x = 0;
+#pragma unroll
+        for (int u = 0; u < 7; ++u) x += (u64)v[u][j] << (8 * u);
+        stg[(threadIdx.x & 31) * 33 + j] = (u32)(x % 134176769u);
+      }
+      acc += stg[(threadIdx.x & 31) * 33];
+    }
+    if (acc == 0xFFFFFFFF) out[1] = acc;
+  } else if (warp == 1) {  // producer
     int s = 0;
     uint32_t ph = 0;
     for (int it = 0; it < iters; ++it) {
@@ -137,14 +156,14 @@ __global__ void __launch_bounds__(64, 1) k(const uint8_t* src, int iters, int ns
   }
 }
 
-template <bool CP, bool PROD, bool ONE = false>
+template <bool CP, bool PROD, bool ONE = false, bool EPI = false>
 void run(const char* name, const uint8_t* src, unsigned long long* d, int sms) {
   const int ns = 7, iters = 3000;
-  const int smem = ns * 20480 + 2048;
-  cudaFuncSetAttribute(k<CP, PROD, ONE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int smem = ns * 20480 + 2048 + 8 * 32 * 33 * 4;
+  cudaFuncSetAttribute(k<CP, PROD, ONE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (int rep = 0; rep < 2; ++rep) {
     cudaMemset(d, 0, 8);
-    k<CP, PROD, ONE><<<sms, 64, smem>>>(src, iters, ns, d);
+    k<CP, PROD, ONE, EPI><<<sms, EPI ? 320 : 64, smem>>>(src, iters, ns, d);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       printf("%s: %s\n", name, cudaGetErrorString(e));
@@ -160,7 +179,7 @@ int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   unsigned long long* d;
-  cudaMalloc(&d, 8);
+  cudaMalloc(&d, 16);
   uint8_t* src;
   cudaMalloc(&src, (size_t)1024 * 20480);
   cudaMemset(src, 3, (size_t)1024 * 20480);
@@ -172,5 +191,7 @@ int main() {
   run<false, true, true>("1-thread loop: ring + MMA", src, d, sms);
   run<true, false, true>("1-thread loop: cp + MMA resident", src, d, sms);
   run<false, false, true>("1-thread loop: MMA only resident", src, d, sms);
+  run<true, true, true, true>("1-thread: ring + cp + MMA + epilogue", src, d, sms);
+  run<false, false, true, true>("1-thread: MMA only + epilogue", src, d, sms);
   return 0;
 }
