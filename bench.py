@@ -263,14 +263,18 @@ def run_ours(args, rank, world, local_rank):
         from paper_2604_04696_b200 import client
 
         coords = [(int(rng.integers(0, d0)), int(rng.integers(0, d1))) for _ in range(B)]
-        queries = np.concatenate([client.queries(ctx, params, client.keygen(ctx, params, b, d0, d1, seed=7000 + b),
-                                                 d0, d1, [coords[b]], seed=9000 + b) for b in range(B)])
+        if args.clients == "single":  # one client's B queries (the reference's run_bench, src/server.py:416-417)
+            sk = client.keygen(ctx, params, 0, d0, d1, seed=7000)
+            queries = client.queries(ctx, params, sk, d0, d1, coords, seed=9000)
+        else:
+            queries = np.concatenate([client.queries(ctx, params, client.keygen(ctx, params, b, d0, d1, seed=7000 + b),
+                                                     d0, d1, [coords[b]], seed=9000 + b) for b in range(B)])
     else:
         evks, rgsw, queries = synthetic_material(G, params, B, stages, rng)
         for b in range(B):
             nat.check(lib.gpir_keys_put(ctx.h, b, nat.ptr(np.ascontiguousarray(evks[b])), stages,
                                         nat.ptr(np.ascontiguousarray(rgsw[b]))), "keys")
-    slots = np.arange(B, dtype=np.int32)
+    slots = np.zeros(B, dtype=np.int32) if args.clients == "single" else np.arange(B, dtype=np.int32)
     words = queries.size
     d_q = torch.from_numpy(queries.view(np.int32).reshape(-1)).to(f"cuda:{dev}")
     d_o = torch.empty_like(d_q)
@@ -367,14 +371,16 @@ def run_ours(args, rank, world, local_rank):
         "metric": "PIR queries/sec (batched)", "value": qps, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 (mod-q, 64-bit lazy products)",
-        "data": ("synthetic random records; B distinct clients' keys and queries generated on the GPU "
-                 "(paper_2604_04696_b200.client)" if args.material == "gpu" else
+        "data": (f"synthetic random records; {'B distinct clients' if args.clients == 'distinct' else 'one client'}"
+                 "'s keys and queries generated on the GPU (paper_2604_04696_b200.client)".replace("clients's", "clients'")
+                 if args.material == "gpu" else
                  "synthetic (random records, uniform-random key/query material)"),
         "config": {"workload": desc, "d0": d0, "d1": d1, "global_batch": B * world, "per_gpu_batch": B,
                    "record_bytes": rb, "plain_bits": pb, "encoded_db_bytes": d0 * d1 * KN * 4,
                    "l2": f"inputs larger than L2 ({d0 * d1 * KN * 4 >> 30} GiB DB streamed by RowSel every step)",
                    "cuda_graph": "timed steps replay the pipeline as a CUDA graph (library default, recorded during "
                                  "warm-up); phases_ms come from eager passes with per-phase events",
+                   "clients": f"{B} distinct" if args.clients == "distinct" else "1 (all B queries from one client)",
                    "parallelism": "replica" if world > 1 else "single",
                    "plan_eq": "".join("oFSH"[v] for v in em[:stages]),
                    "plan_ct": "".join("oFSH"[v] for v in cm[:max(d1.bit_length() - 1, 0)]),
@@ -490,6 +496,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--material", default="gpu", choices=["gpu", "uniform"],
                     help="client keys/queries: real ones generated on the GPU, or uniform-random residues")
+    ap.add_argument("--clients", default="distinct", choices=["distinct", "single"],
+                    help="B distinct clients (worst-case key traffic, default) or one client's B queries")
     ap.add_argument("--strategy", default="replica", choices=["replica", "rowshard", "colshard"],
                     help="multi-GPU mode: replica (DB copy + own batch per GPU), rowshard (north-star DB row "
                          "shards, modular-add combine) or colshard (DB column shards, all-gather)")
