@@ -38,6 +38,15 @@ CONFIGS = {
 }
 
 
+def config_of(args):
+    """The BASELINE config, with the batch overridden by --batch (a sweep at the same DB geometry)."""
+    d0, d1, B, rb, pb, desc = CONFIGS[args.config]
+    if getattr(args, "batch", 0):
+        desc = f"{desc.split(', batch')[0]}, batch {args.batch} (sweep; the config's own batch is {B})"
+        B = args.batch
+    return d0, d1, B, rb, pb, desc
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -223,7 +232,7 @@ def cpu_reference(cfg_id, steps, warmup_cap=1):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    d0, d1, B, rb, pb, desc = CONFIGS[args.config]
+    d0, d1, B, rb, pb, desc = config_of(args)
     qps, sec, cores, sample = cpu_reference(args.config, args.steps)
     tr = ncu_traffic() if args.config == 2 else None  # the committed capture is of the config-2 launch
     line = {
@@ -248,7 +257,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = local_rank
-    d0, d1, B, rb, pb, desc = CONFIGS[args.config]
+    d0, d1, B, rb, pb, desc = config_of(args)
     params = G.HeParams(G.default_basis(4096), pb)
     cfg = G.DbConfig(d0, d1, rb)
     rng = np.random.default_rng(1000 + rank)
@@ -422,7 +431,7 @@ def run_sharded(args, rank, world, local_rank):
                                                answer_row_sharded)
 
     torch.cuda.set_device(local_rank)
-    d0, d1, B, rb, pb, desc = CONFIGS[args.config]
+    d0, d1, B, rb, pb, desc = config_of(args)
     col = args.strategy == "colshard"
     if B % world or (d1 if col else d0) % world:
         raise SystemExit(f"batch {B} / {'d1' if col else 'd0'} do not split over {world} ranks")
@@ -496,6 +505,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--material", default="gpu", choices=["gpu", "uniform"],
                     help="client keys/queries: real ones generated on the GPU, or uniform-random residues")
+    ap.add_argument("--batch", type=int, default=0, help="override the config's batch size (batch sweeps)")
     ap.add_argument("--clients", default="distinct", choices=["distinct", "single"],
                     help="B distinct clients (worst-case key traffic, default) or one client's B queries")
     ap.add_argument("--strategy", default="replica", choices=["replica", "rowshard", "colshard"],
