@@ -23,7 +23,7 @@
 
 // hybrid planner thresholds (nodes / ciphertexts per stage, whole batch)
 static constexpr size_t kEqStageNodes = 2048;
-static constexpr size_t kXpStageCts = 256;
+static constexpr size_t kXpStageCts = 64;  // r1g: ColTor levels of 64-128 pairs are faster stage-level
 
 using namespace gpir;
 

@@ -136,9 +136,9 @@ def choose_mode(working_set_bytes: int, hw: HardwareModel) -> ExecMode:
 
 
 # B200 thresholds of the occupancy rule, measured per stage at config 2
-# (profiles/r1_plans.md); identical to kEqStageNodes / kXpStageCts in gpir.cu
+# (profiles/r1_plans.md, r1g_plans.md); identical to kEqStageNodes / kXpStageCts in gpir.cu
 EQ_STAGE_NODES = 2048
-XP_STAGE_CTS = 256
+XP_STAGE_CTS = 64
 
 
 def choose_mode_occupancy(nodes_in_batch: int, hw: HardwareModel, phase: "Phase | None" = None) -> ExecMode:

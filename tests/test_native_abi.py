@@ -86,7 +86,7 @@ def test_planner_laws():
     modes = "".join("F" if s.mode is G.ExecMode.STAGE_LEVEL else "o" for s in plan.expand_stages)
     assert modes == "ooooooFFF"   # stage-level once B * nodes >= 2048 (measured crossover, profiles/r1_plans.md)
     cmodes = "".join("F" if s.mode is G.ExecMode.STAGE_LEVEL else "o" for s in plan.coltor_stages)
-    assert cmodes == "FFFooo"     # ColTor: stage-level while B * pairs >= 256, then operation-level
+    assert cmodes == "FFFFFo"     # ColTor: stage-level while B * pairs >= 64, then operation-level (r1g_plans.md)
     ref_rule = G.build_plan(G.DbConfig(16, 16, 16384), p, 1, hw, rule="working_set")
     assert all(s.mode is G.ExecMode.OPERATION_LEVEL for s in ref_rule.expand_stages + ref_rule.coltor_stages)
 
