@@ -423,7 +423,8 @@ struct Engine {
       return 0;
     }
     const size_t per = (size_t)K * N + (size_t)ELL * N + (mode == 3 ? 0 : (size_t)ELL * K * N);
-    const size_t chunk = op_chunk(per);
+    static const size_t chunk_env = getenv("GPIR_OP_CHUNK") ? (size_t)atol(getenv("GPIR_OP_CHUNK")) : 0;
+    const size_t chunk = chunk_env ? chunk_env : op_chunk(per);
     const size_t nodes = (size_t)B * C;
     const size_t cn = std::min(chunk, nodes);
     if ((rc = c->ws_coeff.ensure(cn * K * N * 4))) return rc;
@@ -450,10 +451,12 @@ struct Engine {
       k_op_digit_ntt<LOGN, K, ELL><<<dim3(nn * (ELL - 1), K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(), c->tb,
                                                                         c->tc);
       CKL();
+      if (g_sprof.fine) g_sprof.mark(s, "  eq_dntt");
       const size_t tm = (size_t)nn * K * N;
       k_op_eq_mac<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(
           state, C, (int)n0, nn, c->ws_dn.as<u32>(), ksk, k_aut, mono, out, Cout, c->tb);
       CKL();
+      if (g_sprof.fine) g_sprof.mark(s, "  eq_mac");
       *launches += 4;
     }
     return 0;
