@@ -22,7 +22,11 @@
 #include "client.cuh"
 
 // hybrid planner thresholds (nodes / ciphertexts per stage, whole batch)
-static constexpr size_t kEqStageNodes = 2048;
+// ExpandQuery: with the node-batched MAC (k_op_eq_mac_nb) the operation-level
+// executor is faster than the stage kernel at every stage size (r1g: eq8 2.73
+// vs 3.02 ms at config 2, ExpandQuery 22.7 vs 25.2 ms at config 3), so the
+// stage-level threshold is out of reach; mode 3 stays selectable per stage.
+static constexpr size_t kEqStageNodes = (size_t)1 << 62;
 static constexpr size_t kXpStageCts = 64;  // r1g: ColTor levels of 64-128 pairs are faster stage-level
 
 using namespace gpir;
@@ -452,9 +456,18 @@ struct Engine {
                                                                         c->tc);
       CKL();
       if (g_sprof.fine) g_sprof.mark(s, "  eq_dntt");
-      const size_t tm = (size_t)nn * K * N;
-      k_op_eq_mac<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(
-          state, C, (int)n0, nn, c->ws_dn.as<u32>(), ksk, k_aut, mono, out, Cout, c->tb);
+      static const int mac_nb = getenv("GPIR_MAC_NB") ? atoi(getenv("GPIR_MAC_NB")) : 8;
+      if (mac_nb == 8 || mac_nb == 16 || mac_nb == 32) {  // NB nodes per thread: key rows loaded once per group
+        const size_t tm = ((size_t)(nn + mac_nb - 1) / mac_nb) * K * N;
+        auto kern = mac_nb == 8 ? k_op_eq_mac_nb<LOGN, K, ELL, 8>
+                    : mac_nb == 16 ? k_op_eq_mac_nb<LOGN, K, ELL, 16> : k_op_eq_mac_nb<LOGN, K, ELL, 32>;
+        kern<<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(state, C, (int)n0, nn, c->ws_dn.as<u32>(), ksk, k_aut,
+                                                           mono, out, Cout, c->tb);
+      } else {
+        const size_t tm = (size_t)nn * K * N;
+        k_op_eq_mac<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(
+            state, C, (int)n0, nn, c->ws_dn.as<u32>(), ksk, k_aut, mono, out, Cout, c->tb);
+      }
       CKL();
       if (g_sprof.fine) g_sprof.mark(s, "  eq_mac");
       *launches += 4;
@@ -517,10 +530,18 @@ struct Engine {
       k_op_digit_ntt<LOGN, K, ELL><<<dim3(2 * nn * (ELL - 1), K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(),
                                                                             c->tb, c->tc);
       CKL();
-      const size_t tm = (size_t)nn * K * N;
-      k_op_xp_mac<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(in, in_b, M, (int)m0, nn, pairs,
-                                                                             c->ws_dn.as<u32>(), rows, out, out_b,
-                                                                             c->tb);
+      static const int xmac_nb = getenv("GPIR_MAC_NB") ? atoi(getenv("GPIR_MAC_NB")) : 8;
+      if (xmac_nb == 8 || xmac_nb == 16) {  // NB cts per thread: key rows loaded once per group
+        const size_t tm = ((size_t)(nn + xmac_nb - 1) / xmac_nb) * K * N;
+        auto kern = xmac_nb == 8 ? k_op_xp_mac_nb<LOGN, K, ELL, 8> : k_op_xp_mac_nb<LOGN, K, ELL, 16>;
+        kern<<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(in, in_b, M, (int)m0, nn, pairs, c->ws_dn.as<u32>(), rows,
+                                                           out, out_b, c->tb);
+      } else {
+        const size_t tm = (size_t)nn * K * N;
+        k_op_xp_mac<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(in, in_b, M, (int)m0, nn, pairs,
+                                                                               c->ws_dn.as<u32>(), rows, out, out_b,
+                                                                               c->tb);
+      }
       CKL();
       *launches += 4;
     }
@@ -747,13 +768,14 @@ struct Engine {
     return 0;
   }
 
-  // B200 hybrid rule (measured per stage at config 2, profiles/r1_plans.md):
-  // the operation-level kernels win while a stage has too few nodes to fill
-  // the GPU with one CTA per node x limb; beyond that the stage-level
-  // executor (mode 3: operation-level iNTT + Dcp feeding the fused digit-NTT
-  // + key-switch MAC kernel) is fastest.  The single-kernel node-fused
-  // executor (mode 1) is limited to 2 CTAs/SM by its 112 KiB of shared
-  // memory and is never the faster choice on B200.
+  // B200 hybrid rule (measured per stage, profiles/r1_plans.md, r1g_plans.md):
+  // ExpandQuery runs operation-level at every stage since the MAC kernel
+  // batches 8 nodes per thread over their shared key rows (k_op_eq_mac_nb);
+  // ColTor and RGSW assembly switch to the stage-level executor (mode 3:
+  // operation-level iNTT + Dcp feeding the fused digit-NTT + key-switch MAC
+  // kernel) from 64 ciphertexts.  The single-kernel node-fused executor
+  // (mode 1) is limited to 2 CTAs/SM by its 112 KiB of shared memory and is
+  // never the faster choice on B200.
   static int eq_default(size_t nodes) { return nodes >= kEqStageNodes ? 3 : 0; }
   static int xp_default(size_t cts) { return cts >= kXpStageCts ? 3 : 0; }
   static int default_mode(size_t nodes) { return eq_default(nodes); }

@@ -667,6 +667,65 @@ __global__ void k_op_eq_mac(const u32* __restrict__ state, int C, int node0, int
   }
 }
 
+// (4a') the same with NB consecutive nodes per thread: the nodes of one query at
+// one stage share their key rows, so each thread loads the 2 ELL key values of
+// its (limb, slot) once for NB nodes (reloading only where the group crosses
+// into the next query) -- the key rows are most of the MAC's memory traffic.
+template <int LOGN, int K, int ELL, int NB>
+__global__ void k_op_eq_mac_nb(const u32* __restrict__ state, int C, int node0, int nodes, const u32* __restrict__ dn,
+                               RowsDesc ksk, u32 k_aut, const uint2* __restrict__ mono, u32* __restrict__ out,
+                               int Cout, Tables tb) {
+  constexpr int N = 1 << LOGN;
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t groups = ((size_t)nodes + NB - 1) / NB;
+  if (g >= groups * K * N) return;
+  const int pos = (int)(g & (N - 1));
+  const int i = (int)((g >> LOGN) % K);
+  const int nd0 = (int)(g / ((size_t)K * N)) * NB;
+  const size_t CT = 2 * (size_t)K * N;
+  const Modulus M = tb.mod[i];
+  const u32 q = M.q;
+  const u32 src_pos = aut_src(pos, k_aut, LOGN);
+  const uint2 w = __ldg(&mono[(size_t)i * N + pos]);
+  int cur_b = -1;
+  u32 ka[ELL], kb[ELL];
+#pragma unroll 1
+  for (int u = 0; u < NB; ++u) {
+    const int nd = nd0 + u;
+    if (nd >= nodes) break;
+    const int gn = node0 + nd;
+    const int b = gn / C, c = gn % C;
+    if (b != cur_b) {
+#pragma unroll
+      for (int j = 0; j < ELL; ++j) {
+        const u32* ra = ksk.row(b, j, ELL, CT) + (size_t)i * N + pos;
+        ka[j] = __ldg(ra);
+        kb[j] = __ldg(ra + (size_t)K * N);
+      }
+      cur_b = b;
+    }
+    const u32* st = state + (size_t)gn * CT;
+    u64 a0 = 0, a1 = 0;
+#pragma unroll
+    for (int j = 0; j < ELL; ++j) {  // digit ELL-1 is folded: its term is tau(a) itself
+      const u32 d = j < ELL - 1 ? __ldg(dn + (((size_t)nd * ELL + j) * K + i) * N + pos) : __ldg(st + (size_t)i * N + src_pos);
+      a0 += (u64)d * ka[j];
+      a1 += (u64)d * kb[j];
+    }
+    const u32 ca = __ldg(st + (size_t)i * N + pos), cb = __ldg(st + (size_t)(K + i) * N + pos);
+    const u32 sa = reduce_u64(a0, M);
+    const u32 sb = mod_add(reduce_u64(a1, M), __ldg(st + (size_t)(K + i) * N + src_pos), q);
+    u32* o0 = out + ((size_t)b * Cout + c) * CT;
+    o0[(size_t)i * N + pos] = mod_add(ca, sa, q);
+    o0[(size_t)(K + i) * N + pos] = mod_add(cb, sb, q);
+    if (c + C < Cout) {
+      u32* o1 = out + ((size_t)b * Cout + c + C) * CT;
+      o1[(size_t)i * N + pos] = csub(mul_shoup(mod_sub(ca, sa, q), w.x, w.y, q), q);
+      o1[(size_t)(K + i) * N + pos] = csub(mul_shoup(mod_sub(cb, sb, q), w.x, w.y, q), q);
+    }
+  }
+}
+
 // (4b) external-product MAC (+ ColTor combine); one thread per (ct, limb, slot).
 template <int LOGN, int K, int ELL>
 __global__ void k_op_xp_mac(const u32* __restrict__ in, size_t in_b, int M_per_b, int m0, int cts, int pairs,
@@ -710,6 +769,70 @@ __global__ void k_op_xp_mac(const u32* __restrict__ in, size_t in_b, int M_per_b
   u32* d = out + (b * out_b + (size_t)m) * CT;
   d[(size_t)i * N + pos] = sa;
   d[(size_t)(K + i) * N + pos] = sb;
+}
+
+// (4b') the same with NB consecutive ciphertexts per thread: the cts of one query
+// (the ColTor pairs of one level, the RGSW-assembly column cts) share their key
+// rows, loaded once per group and reloaded only where it crosses into the next query.
+template <int LOGN, int K, int ELL, int NB>
+__global__ void k_op_xp_mac_nb(const u32* __restrict__ in, size_t in_b, int M_per_b, int m0, int cts, int pairs,
+                               const u32* __restrict__ dn, RowsDesc rows, u32* __restrict__ out, size_t out_b,
+                               Tables tb) {
+  constexpr int N = 1 << LOGN;
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t groups = ((size_t)cts + NB - 1) / NB;
+  if (g >= groups * K * N) return;
+  const int pos = (int)(g & (N - 1));
+  const int i = (int)((g >> LOGN) % K);
+  const int ct0 = (int)(g / ((size_t)K * N)) * NB;
+  const size_t CT = 2 * (size_t)K * N;
+  const Modulus M = tb.mod[i];
+  const u32 q = M.q;
+  int cur_b = -1;
+  u32 ka[2 * ELL], kb[2 * ELL];
+#pragma unroll 1
+  for (int u = 0; u < NB; ++u) {
+    const int ct = ct0 + u;
+    if (ct >= cts) break;
+    const int gm = m0 + ct;
+    const int b = gm / M_per_b, m = gm % M_per_b;
+    if (b != cur_b) {
+#pragma unroll
+      for (int r = 0; r < 2 * ELL; ++r) {
+        const u32* ra = rows.row(b, r, ELL, CT) + (size_t)i * N + pos;
+        ka[r] = __ldg(ra);
+        kb[r] = __ldg(ra + (size_t)K * N);
+      }
+      cur_b = b;
+    }
+    const u32* src = pairs ? in + (b * in_b + 2 * (size_t)m) * CT : in + (b * in_b + (size_t)m) * CT;
+    u64 a0 = 0, a1 = 0;
+#pragma unroll
+    for (int comp = 0; comp < 2; ++comp) {
+#pragma unroll
+      for (int j = 0; j < ELL; ++j) {
+        u32 d;
+        if (j < ELL - 1) {
+          d = __ldg(dn + ((((size_t)ct * 2 + comp) * ELL + j) * K + i) * N + pos);
+        } else {  // folded top digit: this component of the input (or odd - even)
+          const size_t off = (size_t)(comp * K + i) * N + pos;
+          d = __ldg(src + off);
+          if (pairs) d = mod_sub(__ldg(src + CT + off), d, q);
+        }
+        a0 += (u64)d * ka[comp * ELL + j];
+        a1 += (u64)d * kb[comp * ELL + j];
+      }
+    }
+    u32 sa = reduce_u64(a0, M), sb = reduce_u64(a1, M);
+    if (pairs) {
+      const u32* ev = in + (b * in_b + 2 * (size_t)m) * CT;
+      sa = mod_add(sa, __ldg(ev + (size_t)i * N + pos), q);
+      sb = mod_add(sb, __ldg(ev + (size_t)(K + i) * N + pos), q);
+    }
+    u32* d = out + (b * out_b + (size_t)m) * CT;
+    d[(size_t)i * N + pos] = sa;
+    d[(size_t)(K + i) * N + pos] = sb;
+  }
 }
 
 // ---------------------------------------------------------------------------

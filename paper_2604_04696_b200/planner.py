@@ -137,7 +137,7 @@ def choose_mode(working_set_bytes: int, hw: HardwareModel) -> ExecMode:
 
 # B200 thresholds of the occupancy rule, measured per stage at config 2
 # (profiles/r1_plans.md, r1g_plans.md); identical to kEqStageNodes / kXpStageCts in gpir.cu
-EQ_STAGE_NODES = 2048
+EQ_STAGE_NODES = 1 << 62  # r1g: operation-level wins at every ExpandQuery stage (node-batched MAC)
 XP_STAGE_CTS = 64
 
 

@@ -84,7 +84,7 @@ def test_planner_laws():
     assert ws == 5_368_709_120
     plan = G.build_plan(G.DbConfig(256, 64, 8192), p, 32, G.HardwareModel.b200())
     modes = "".join("F" if s.mode is G.ExecMode.STAGE_LEVEL else "o" for s in plan.expand_stages)
-    assert modes == "ooooooFFF"   # stage-level once B * nodes >= 2048 (measured crossover, profiles/r1_plans.md)
+    assert modes == "ooooooooo"   # r1g: operation-level at every ExpandQuery stage (profiles/r1g_plans.md)
     cmodes = "".join("F" if s.mode is G.ExecMode.STAGE_LEVEL else "o" for s in plan.coltor_stages)
     assert cmodes == "FFFFFo"     # ColTor: stage-level while B * pairs >= 64, then operation-level (r1g_plans.md)
     ref_rule = G.build_plan(G.DbConfig(16, 16, 16384), p, 1, hw, rule="working_set")
