@@ -456,8 +456,14 @@ struct Engine {
                                                                         c->tc);
       CKL();
       if (g_sprof.fine) g_sprof.mark(s, "  eq_dntt");
-      static const int mac_nb = getenv("GPIR_MAC_NB") ? atoi(getenv("GPIR_MAC_NB")) : 8;
-      if (mac_nb == 8 || mac_nb == 16 || mac_nb == 32) {  // NB nodes per thread: key rows loaded once per group
+      static const int mac_nb = getenv("GPIR_MAC_NB") ? atoi(getenv("GPIR_MAC_NB")) : 108;
+      if (mac_nb == 4 || mac_nb == 104 || mac_nb == 108) {  // 4 slots per thread (128-bit accesses), NB nodes
+        const int nb = mac_nb == 4 ? 4 : mac_nb - 100;
+        const size_t tm = ((size_t)(nn + nb - 1) / nb) * K * (N / 4);
+        auto kern = nb == 4 ? k_op_eq_mac_nb4<LOGN, K, ELL, 4> : k_op_eq_mac_nb4<LOGN, K, ELL, 8>;
+        kern<<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(state, C, (int)n0, nn, c->ws_dn.as<u32>(), ksk, k_aut,
+                                                           mono, out, Cout, c->tb);
+      } else if (mac_nb == 8 || mac_nb == 16 || mac_nb == 32) {  // NB nodes per thread: key rows loaded once per group
         const size_t tm = ((size_t)(nn + mac_nb - 1) / mac_nb) * K * N;
         auto kern = mac_nb == 8 ? k_op_eq_mac_nb<LOGN, K, ELL, 8>
                     : mac_nb == 16 ? k_op_eq_mac_nb<LOGN, K, ELL, 16> : k_op_eq_mac_nb<LOGN, K, ELL, 32>;
@@ -530,8 +536,16 @@ struct Engine {
       k_op_digit_ntt<LOGN, K, ELL><<<dim3(2 * nn * (ELL - 1), K), T, 0, s>>>(c->ws_dig.as<int>(), c->ws_dn.as<u32>(),
                                                                             c->tb, c->tc);
       CKL();
-      static const int xmac_nb = getenv("GPIR_MAC_NB") ? atoi(getenv("GPIR_MAC_NB")) : 8;
-      if (xmac_nb == 8 || xmac_nb == 16) {  // NB cts per thread: key rows loaded once per group
+      // 8 cts per thread, one slot each: the 4-slot variant needs 2 x 4 ELL key registers (130 in all) and
+      // loses more to occupancy than it saves in load instructions (ColTor level 0: 0.884 vs 0.798 ms)
+      static const int xmac_nb = getenv("GPIR_XMAC_NB") ? atoi(getenv("GPIR_XMAC_NB")) : 8;
+      if (xmac_nb == 104 || xmac_nb == 108) {  // 4 slots per thread (128-bit accesses), NB cts
+        const int nb = xmac_nb - 100;
+        const size_t tm = ((size_t)(nn + nb - 1) / nb) * K * (N / 4);
+        auto kern = nb == 4 ? k_op_xp_mac_nb4<LOGN, K, ELL, 4> : k_op_xp_mac_nb4<LOGN, K, ELL, 8>;
+        kern<<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(in, in_b, M, (int)m0, nn, pairs, c->ws_dn.as<u32>(), rows,
+                                                           out, out_b, c->tb);
+      } else if (xmac_nb == 8 || xmac_nb == 16) {  // NB cts per thread: key rows loaded once per group
         const size_t tm = ((size_t)(nn + xmac_nb - 1) / xmac_nb) * K * N;
         auto kern = xmac_nb == 8 ? k_op_xp_mac_nb<LOGN, K, ELL, 8> : k_op_xp_mac_nb<LOGN, K, ELL, 16>;
         kern<<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(in, in_b, M, (int)m0, nn, pairs, c->ws_dn.as<u32>(), rows,

@@ -622,7 +622,9 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
   const int* src = digits + (size_t)pe * N;
   const u32 q = tb.mod[i].q;
   u32* dst = dn + ((size_t)pe * K + i) * N;
-  ntt_fwd<LOGN>(
+  // lazy outputs (< (2 log n + 1) q < 2^32): the 64-bit MACs take them as they are
+  // (ELL terms of < 25 q * q per accumulator, < 2^62)
+  ntt_fwd<LOGN, true>(
       ns, tb.fwd + (size_t)i * N, tc.f[i], tb.mod[i], [&](int j) -> u32 { return lift(__ldg(src + j), q); },
       [&](int i0, const u32(&x)[16]) { st16(dst + i0, x); });
 }
@@ -722,6 +724,90 @@ __global__ void k_op_eq_mac_nb(const u32* __restrict__ state, int C, int node0, 
       u32* o1 = out + ((size_t)b * Cout + c + C) * CT;
       o1[(size_t)i * N + pos] = csub(mul_shoup(mod_sub(ca, sa, q), w.x, w.y, q), q);
       o1[(size_t)(K + i) * N + pos] = csub(mul_shoup(mod_sub(cb, sb, q), w.x, w.y, q), q);
+    }
+  }
+}
+
+// (4a'') node-batched MAC with 4 consecutive slots per thread (128-bit loads and
+// stores for everything but the automorphism gathers).
+template <int LOGN, int K, int ELL, int NB>
+__global__ void __launch_bounds__(256) k_op_eq_mac_nb4(const u32* __restrict__ state, int C, int node0, int nodes,
+                                                       const u32* __restrict__ dn, RowsDesc ksk, u32 k_aut,
+                                                       const uint2* __restrict__ mono, u32* __restrict__ out, int Cout,
+                                                       Tables tb) {
+  constexpr int N = 1 << LOGN;
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t groups = ((size_t)nodes + NB - 1) / NB;
+  if (g >= groups * K * (N / 4)) return;
+  const int pos = (int)(g & (N / 4 - 1)) * 4;
+  const int i = (int)((g / (N / 4)) % K);
+  const int nd0 = (int)(g / ((size_t)K * (N / 4))) * NB;
+  const size_t CT = 2 * (size_t)K * N;
+  const Modulus M = tb.mod[i];
+  const u32 q = M.q;
+  u32 src_pos[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) src_pos[r] = aut_src(pos + r, k_aut, LOGN);
+  int cur_b = -1;
+  uint4 ka[ELL], kb[ELL];
+#pragma unroll 1
+  for (int u = 0; u < NB; ++u) {
+    const int nd = nd0 + u;
+    if (nd >= nodes) break;
+    const int gn = node0 + nd;
+    const int b = gn / C, c = gn % C;
+    if (b != cur_b) {
+#pragma unroll
+      for (int j = 0; j < ELL; ++j) {
+        const u32* ra = ksk.row(b, j, ELL, CT) + (size_t)i * N + pos;
+        ka[j] = __ldg(reinterpret_cast<const uint4*>(ra));
+        kb[j] = __ldg(reinterpret_cast<const uint4*>(ra + (size_t)K * N));
+      }
+      cur_b = b;
+    }
+    const u32* st = state + (size_t)gn * CT;
+    u64 a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < ELL; ++j) {  // digit ELL-1 is folded: its term is tau(a) itself
+      u32 d[4];
+      if (j < ELL - 1) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(dn + (((size_t)nd * ELL + j) * K + i) * N + pos));
+        d[0] = v.x, d[1] = v.y, d[2] = v.z, d[3] = v.w;
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) d[r] = __ldg(st + (size_t)i * N + src_pos[r]);
+      }
+      const u32 kav[4] = {ka[j].x, ka[j].y, ka[j].z, ka[j].w}, kbv[4] = {kb[j].x, kb[j].y, kb[j].z, kb[j].w};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        a0[r] += (u64)d[r] * kav[r];
+        a1[r] += (u64)d[r] * kbv[r];
+      }
+    }
+    const uint4 ca4 = __ldg(reinterpret_cast<const uint4*>(st + (size_t)i * N + pos));
+    const uint4 cb4 = __ldg(reinterpret_cast<const uint4*>(st + (size_t)(K + i) * N + pos));
+    const u32 ca[4] = {ca4.x, ca4.y, ca4.z, ca4.w}, cb[4] = {cb4.x, cb4.y, cb4.z, cb4.w};
+    u32 xa[4], xb[4], ya[4], yb[4];
+    const bool second = c + C < Cout;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const u32 sa = reduce_u64(a0[r], M);
+      const u32 sb = mod_add(reduce_u64(a1[r], M), __ldg(st + (size_t)(K + i) * N + src_pos[r]), q);
+      xa[r] = mod_add(ca[r], sa, q);
+      xb[r] = mod_add(cb[r], sb, q);
+      if (second) {
+        const uint2 w = __ldg(&mono[(size_t)i * N + pos + r]);
+        ya[r] = csub(mul_shoup(mod_sub(ca[r], sa, q), w.x, w.y, q), q);
+        yb[r] = csub(mul_shoup(mod_sub(cb[r], sb, q), w.x, w.y, q), q);
+      }
+    }
+    u32* o0 = out + ((size_t)b * Cout + c) * CT;
+    *reinterpret_cast<uint4*>(o0 + (size_t)i * N + pos) = make_uint4(xa[0], xa[1], xa[2], xa[3]);
+    *reinterpret_cast<uint4*>(o0 + (size_t)(K + i) * N + pos) = make_uint4(xb[0], xb[1], xb[2], xb[3]);
+    if (second) {
+      u32* o1 = out + ((size_t)b * Cout + c + C) * CT;
+      *reinterpret_cast<uint4*>(o1 + (size_t)i * N + pos) = make_uint4(ya[0], ya[1], ya[2], ya[3]);
+      *reinterpret_cast<uint4*>(o1 + (size_t)(K + i) * N + pos) = make_uint4(yb[0], yb[1], yb[2], yb[3]);
     }
   }
 }
@@ -832,6 +918,78 @@ __global__ void k_op_xp_mac_nb(const u32* __restrict__ in, size_t in_b, int M_pe
     u32* d = out + (b * out_b + (size_t)m) * CT;
     d[(size_t)i * N + pos] = sa;
     d[(size_t)(K + i) * N + pos] = sb;
+  }
+}
+
+// (4b'') node-batched external-product MAC with 4 consecutive slots per thread.
+template <int LOGN, int K, int ELL, int NB>
+__global__ void __launch_bounds__(256) k_op_xp_mac_nb4(const u32* __restrict__ in, size_t in_b, int M_per_b, int m0,
+                                                       int cts, int pairs, const u32* __restrict__ dn, RowsDesc rows,
+                                                       u32* __restrict__ out, size_t out_b, Tables tb) {
+  constexpr int N = 1 << LOGN;
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t groups = ((size_t)cts + NB - 1) / NB;
+  if (g >= groups * K * (N / 4)) return;
+  const int pos = (int)(g & (N / 4 - 1)) * 4;
+  const int i = (int)((g / (N / 4)) % K);
+  const int ct0 = (int)(g / ((size_t)K * (N / 4))) * NB;
+  const size_t CT = 2 * (size_t)K * N;
+  const Modulus M = tb.mod[i];
+  const u32 q = M.q;
+  int cur_b = -1;
+  uint4 ka[2 * ELL], kb[2 * ELL];
+#pragma unroll 1
+  for (int u = 0; u < NB; ++u) {
+    const int ct = ct0 + u;
+    if (ct >= cts) break;
+    const int gm = m0 + ct;
+    const int b = gm / M_per_b, m = gm % M_per_b;
+    if (b != cur_b) {
+#pragma unroll
+      for (int r = 0; r < 2 * ELL; ++r) {
+        const u32* ra = rows.row(b, r, ELL, CT) + (size_t)i * N + pos;
+        ka[r] = __ldg(reinterpret_cast<const uint4*>(ra));
+        kb[r] = __ldg(reinterpret_cast<const uint4*>(ra + (size_t)K * N));
+      }
+      cur_b = b;
+    }
+    const u32* src = pairs ? in + (b * in_b + 2 * (size_t)m) * CT : in + (b * in_b + (size_t)m) * CT;
+    u64 a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int comp = 0; comp < 2; ++comp) {
+#pragma unroll
+      for (int j = 0; j < ELL; ++j) {
+        uint4 v;
+        if (j < ELL - 1) {
+          v = __ldg(reinterpret_cast<const uint4*>(dn + ((((size_t)ct * 2 + comp) * ELL + j) * K + i) * N + pos));
+        } else {  // folded top digit: this component of the input (or odd - even)
+          const size_t off = (size_t)(comp * K + i) * N + pos;
+          v = __ldg(reinterpret_cast<const uint4*>(src + off));
+          if (pairs) {
+            const uint4 o = __ldg(reinterpret_cast<const uint4*>(src + CT + off));
+            v = make_uint4(mod_sub(o.x, v.x, q), mod_sub(o.y, v.y, q), mod_sub(o.z, v.z, q), mod_sub(o.w, v.w, q));
+          }
+        }
+        const uint4 kr = ka[comp * ELL + j], ks = kb[comp * ELL + j];
+        a0[0] += (u64)v.x * kr.x, a0[1] += (u64)v.y * kr.y, a0[2] += (u64)v.z * kr.z, a0[3] += (u64)v.w * kr.w;
+        a1[0] += (u64)v.x * ks.x, a1[1] += (u64)v.y * ks.y, a1[2] += (u64)v.z * ks.z, a1[3] += (u64)v.w * ks.w;
+      }
+    }
+    u32 sa[4], sb[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) sa[r] = reduce_u64(a0[r], M), sb[r] = reduce_u64(a1[r], M);
+    if (pairs) {
+      const u32* ev = in + (b * in_b + 2 * (size_t)m) * CT;
+      const uint4 ea = __ldg(reinterpret_cast<const uint4*>(ev + (size_t)i * N + pos));
+      const uint4 eb = __ldg(reinterpret_cast<const uint4*>(ev + (size_t)(K + i) * N + pos));
+      sa[0] = mod_add(sa[0], ea.x, q), sa[1] = mod_add(sa[1], ea.y, q), sa[2] = mod_add(sa[2], ea.z, q),
+      sa[3] = mod_add(sa[3], ea.w, q);
+      sb[0] = mod_add(sb[0], eb.x, q), sb[1] = mod_add(sb[1], eb.y, q), sb[2] = mod_add(sb[2], eb.z, q),
+      sb[3] = mod_add(sb[3], eb.w, q);
+    }
+    u32* d = out + (b * out_b + (size_t)m) * CT;
+    *reinterpret_cast<uint4*>(d + (size_t)i * N + pos) = make_uint4(sa[0], sa[1], sa[2], sa[3]);
+    *reinterpret_cast<uint4*>(d + (size_t)(K + i) * N + pos) = make_uint4(sb[0], sb[1], sb[2], sb[3]);
   }
 }
 
