@@ -829,7 +829,8 @@ struct Engine {
     // RGSW assembly (src/protocol.py:383-409): a-rows = col_cts ⊡ RGSW(s)
     if (bits_tree > 0) {
       const int M = (int)(bits_tree * ELL);
-      const int mode = xp_default((size_t)B * M);
+      static const int rgsw_env = getenv("GPIR_RGSW_MODE") ? atoi(getenv("GPIR_RGSW_MODE")) : -1;
+      const int mode = rgsw_env >= 0 ? rgsw_env : xp_default((size_t)B * M);
       if ((rc = ext_product(c, leaves + (size_t)d0 * CT, total, B, M, 0, c->ws_arows.as<u32>(), (size_t)M,
                             skrgsw_rows(c, kslot), mode, s, &launches)))
         return rc;
