@@ -457,10 +457,11 @@ struct Engine {
       CKL();
       if (g_sprof.fine) g_sprof.mark(s, "  eq_dntt");
       static const int mac_nb = getenv("GPIR_MAC_NB") ? atoi(getenv("GPIR_MAC_NB")) : 108;
-      if (mac_nb == 4 || mac_nb == 104 || mac_nb == 108) {  // 4 slots per thread (128-bit accesses), NB nodes
+      if (mac_nb == 4 || mac_nb == 104 || mac_nb == 108 || mac_nb == 116) {  // 4 slots per thread, NB nodes
         const int nb = mac_nb == 4 ? 4 : mac_nb - 100;
         const size_t tm = ((size_t)(nn + nb - 1) / nb) * K * (N / 4);
-        auto kern = nb == 4 ? k_op_eq_mac_nb4<LOGN, K, ELL, 4> : k_op_eq_mac_nb4<LOGN, K, ELL, 8>;
+        auto kern = nb == 4 ? k_op_eq_mac_nb4<LOGN, K, ELL, 4>
+                    : nb == 8 ? k_op_eq_mac_nb4<LOGN, K, ELL, 8> : k_op_eq_mac_nb4<LOGN, K, ELL, 16>;
         kern<<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(state, C, (int)n0, nn, c->ws_dn.as<u32>(), ksk, k_aut,
                                                            mono, out, Cout, c->tb);
       } else if (mac_nb == 8 || mac_nb == 16 || mac_nb == 32) {  // NB nodes per thread: key rows loaded once per group
