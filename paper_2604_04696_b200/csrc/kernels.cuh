@@ -622,10 +622,28 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
   const int* src = digits + (size_t)pe * N;
   const u32 q = tb.mod[i].q;
   u32* dst = dn + ((size_t)pe * K + i) * N;
+#ifndef DNTT_STAGE
+#define DNTT_STAGE 1
+#endif
+#if DNTT_STAGE
+  // the digit row arrives by one bulk copy into the exchange buffer the transform does not use
+  __shared__ uint64_t bar;
+  const int* stage = reinterpret_cast<const int*>(xbuf + N);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, N * 4u);
+    bulk_g2s(xbuf + N, src, N * 4u, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+#else
+  const int* stage = src;
+#endif
   // lazy outputs (< (2 log n + 1) q < 2^32): the 64-bit MACs take them as they are
   // (ELL terms of < 25 q * q per accumulator, < 2^62)
   ntt_fwd<LOGN, true>(
-      ns, tb.fwd + (size_t)i * N, tc.f[i], tb.mod[i], [&](int j) -> u32 { return lift(__ldg(src + j), q); },
+      ns, tb.fwd + (size_t)i * N, tc.f[i], tb.mod[i], [&](int j) -> u32 { return lift(stage[j], q); },
       [&](int i0, const u32(&x)[16]) { st16(dst + i0, x); });
 }
 
