@@ -287,7 +287,8 @@ def run_ours(args, rank, world, local_rank):
     words = queries.size
     d_q = torch.from_numpy(queries.view(np.int32).reshape(-1)).to(f"cuda:{dev}")
     d_o = torch.empty_like(d_q)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: the legacy default stream (handle 0) cannot be graph-captured
+    stream = torch.cuda.Stream(dev)
     sptr = C.c_void_p(stream.cuda_stream)
     em = np.zeros(16, np.uint8)
     cm = np.zeros(16, np.uint8)

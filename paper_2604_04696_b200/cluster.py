@@ -172,7 +172,10 @@ class CudaRowShard:
         self.stream = torch.cuda.current_stream(device)
 
     def _sp(self):
-        return C.c_void_p(self.stream.cuda_stream)
+        # torch's legacy default stream is handle 0, which the C ABI reads as "the
+        # context's private stream"; pass cudaStreamLegacy (1) so the library's
+        # launches stay ordered with the collectives torch queued on stream 0
+        return C.c_void_p(self.stream.cuda_stream or 1)
 
     def swap01(self, t):
         return t.transpose(0, 1).contiguous()
@@ -240,7 +243,10 @@ class CudaColShard:
         self.stream = torch.cuda.current_stream(device)
 
     def _sp(self):
-        return C.c_void_p(self.stream.cuda_stream)
+        # torch's legacy default stream is handle 0, which the C ABI reads as "the
+        # context's private stream"; pass cudaStreamLegacy (1) so the library's
+        # launches stay ordered with the collectives torch queued on stream 0
+        return C.c_void_p(self.stream.cuda_stream or 1)
 
     def _new(self, *shape):
         return self.torch.empty(shape, dtype=self.torch.int32, device=f"cuda:{self.device}")

@@ -133,6 +133,7 @@ struct gpir_ctx {
   uint32_t sh_B = 0, sh_d0 = 0, sh_d1 = 0, sh_total = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[12];
+  cudaEvent_t ev_legacy = nullptr;  // orders the private stream after the legacy default stream (pick_stream)
   // CUDA graphs of the device pipeline (answer_dev), keyed by everything the
   // captured launches bake in; the first call of a key runs eagerly (lazy
   // allocations, DB byte-plane packing), the second captures, later ones replay
@@ -277,6 +278,17 @@ static int build_tables(gpir_ctx* c) {
 // ---------------------------------------------------------------------------
 // geometry (src/planner.py:153-173)
 
+// The stream a device-pointer entry point runs on: the caller's, or (NULL) the
+// context's private stream ordered after all work already queued on the legacy
+// default stream -- e.g. a collective or copy torch issued on stream 0 -- so
+// NULL behaves like the default stream for the caller (the call then also
+// synchronises before returning).
+static cudaStream_t pick_stream(gpir_ctx* c, void* stream) {
+  if (stream) return (cudaStream_t)stream;
+  if (cudaEventRecord(c->ev_legacy, cudaStreamLegacy) == cudaSuccess) cudaStreamWaitEvent(c->stream, c->ev_legacy, 0);
+  return c->stream;
+}
+
 static uint32_t ilog2(uint32_t v) {
   uint32_t r = 0;
   while ((1u << r) < v) ++r;
@@ -398,8 +410,10 @@ struct Engine {
   }
 
   // one ExpandQuery stage: state (B, C) -> out (B, Cout)
+  // a8f (operation-level mode only): write the row leaves (outputs c < d0) as
+  // RowSel byte planes in that layout instead of u32 words (k_op_eq_mac_a8)
   static int expand_stage(gpir_ctx* c, const u32* state, int B, int C, u32* out, int Cout, int t, RowsDesc ksk,
-                          int mode, cudaStream_t s, uint32_t* launches) {
+                          int mode, cudaStream_t s, uint32_t* launches, const A8Desc* a8f = nullptr, int d0 = 0) {
     const u32 k_aut = (u32)(N >> t) + 1;
     const uint2* mono = c->mono.as<uint2>() + (size_t)t * K * N;
     int rc;
@@ -428,7 +442,8 @@ struct Engine {
     }
     const size_t per = (size_t)K * N + (size_t)ELL * N + (mode == 3 ? 0 : (size_t)ELL * K * N);
     static const size_t chunk_env = getenv("GPIR_OP_CHUNK") ? (size_t)atol(getenv("GPIR_OP_CHUNK")) : 0;
-    const size_t chunk = chunk_env ? chunk_env : op_chunk(per);
+    size_t chunk = chunk_env ? chunk_env : op_chunk(per);
+    if (chunk >= 16) chunk &= ~(size_t)15;  // node groups of the batched MACs never straddle a chunk
     const size_t nodes = (size_t)B * C;
     const size_t cn = std::min(chunk, nodes);
     if ((rc = c->ws_coeff.ensure(cn * K * N * 4))) return rc;
@@ -457,7 +472,11 @@ struct Engine {
       CKL();
       if (g_sprof.fine) g_sprof.mark(s, "  eq_dntt");
       static const int mac_nb = getenv("GPIR_MAC_NB") ? atoi(getenv("GPIR_MAC_NB")) : 108;
-      if (mac_nb == 4 || mac_nb == 104 || mac_nb == 108 || mac_nb == 116) {  // 4 slots per thread, NB nodes
+      if (a8f) {  // last stage: row leaves straight into the RowSel A operand
+        const size_t tm = (size_t)(nn / 16) * K * N;
+        k_op_eq_mac_a8<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(
+            state, C, (int)n0, nn, c->ws_dn.as<u32>(), ksk, k_aut, mono, out, Cout, c->tb, *a8f, d0);
+      } else if (mac_nb == 4 || mac_nb == 104 || mac_nb == 108 || mac_nb == 116) {  // 4 slots per thread, NB nodes
         const int nb = mac_nb == 4 ? 4 : mac_nb - 100;
         const size_t tm = ((size_t)(nn + nb - 1) / nb) * K * (N / 4);
         auto kern = nb == 4 ? k_op_eq_mac_nb4<LOGN, K, ELL, 4>
@@ -598,62 +617,166 @@ struct Engine {
     return 0;
   }
 
-  // RowSel: tensor-core path (byte-plane u8 GEMMs, rowsel_tc.cuh) when the
-  // shape allows, else the CUDA-core kernel.  ev_mid (if non-null) is
-  // recorded between operand packing and the GEMM.
-  static int rowsel(gpir_ctx* c, const u32* leaves, size_t a_b_words, int B, gpir_db* db, u32* sel,
-                    cudaStream_t s, uint32_t* launches, cudaEvent_t ev_mid = nullptr) {
+  // RowSel execution plan for a (B, db) shape:
+  //   kind 0: CUDA cores (k_rowsel_cc, d0 > 1024 or engine 1);
+  //   kind 1: tensor cores, operands streamed per K chunk (k_rowsel_tc: M = 64 tiles, or d0 > 256);
+  //   kind 2: tensor cores, A resident in TMEM (k_rowsel_tk: 2B > 64, d0 <= 256).
+  // The A operand's byte-plane layout (a8) is fixed here so the last ExpandQuery
+  // stage can write it directly (k_op_eq_mac_a8).
+  struct RsPlan {
+    int kind = 0;
+    int M = 0, RA = 0, mtiles = 0, NT = 0, KC = 0, nchunks = 0, ntiles = 0, PST = 0;
+    A8Desc a8{};
+    size_t a8_bytes = 0;
+  };
+  static RsPlan rs_plan(gpir_ctx* c, int B, const gpir_db* db) {
+    RsPlan r;
     const int KN = K * N;
-    int rc;
-    if (tc_eligible(c, B, db)) {
-      const int M = 2 * B;
-      const int RA = M <= 128 ? M : 128;  // rows per A tile
-      const int mtiles = (M + RA - 1) / RA;
-      const bool m64 = RA <= 64;
+    r.M = 2 * B;
+    if (!tc_eligible(c, B, db)) return r;
+    static const int tk_env = getenv("GPIR_TK") ? atoi(getenv("GPIR_TK")) : 1;
+    const bool tk = tk_env && r.M > 64 && db->d0 <= 256;
+    if (tk) {
+      r.kind = 2;
+      r.RA = 128;
+      r.mtiles = (r.M + 127) / 128;
+      r.NT = TK_NT;
+      r.KC = ((int)db->d0 + 31) & ~31;
+      r.nchunks = 1;
+      r.ntiles = ((int)db->d1 + TK_NT - 1) / TK_NT;
+    } else {
+      r.kind = 1;
+      r.RA = r.M <= 128 ? r.M : 128;
+      r.mtiles = (r.M + r.RA - 1) / r.RA;
+      const bool m64 = r.RA <= 64;
       static const int nt_env = getenv("GPIR_TC_NT") ? atoi(getenv("GPIR_TC_NT")) : 0;
-      static const int ord_env = getenv("GPIR_TC_ORDER") ? atoi(getenv("GPIR_TC_ORDER")) : -1;
       // N = 64 columns per tile when M = 64 (both TMEM accumulator buffers
       // still fit, lane-interleaved); M = 128 tiles use N = 32 with two
       // 7 x 32-column buffers so the epilogue overlaps the next item's MMAs
-      const int NT = (nt_env == 32 || nt_env == 64) ? nt_env : (m64 && db->d1 >= 64 ? 64 : 32);
+      r.NT = (nt_env == 32 || nt_env == 64) ? nt_env : (m64 && db->d1 >= 64 ? 64 : 32);
       static const int pst_env = getenv("GPIR_TC_PST") ? atoi(getenv("GPIR_TC_PST")) : 0;
       // p per staged epilogue flush: the staging buffer competes with the TMA
       // pipeline for shared memory, so the M64 x N64 tile stages 4 p (4 stages
       // in flight) rather than 8 (2 stages)
-      const int PST = (!m64 && NT == 64)                           ? (pst_env == 2 ? 2 : 4)
-                      : (pst_env == 2 || pst_env == 4 || pst_env == 8) ? pst_env
-                      : m64                                      ? (NT == 64 ? 4 : 8)
-                                                                 : 4;
-      const int KC = m64 ? 64 : 32;
-      const int nchunks = ((int)db->d0 + KC - 1) / KC;
-      const int ntiles = ((int)db->d1 + NT - 1) / NT;
-      if (db->d8_nt != NT || db->d8_kc != KC) {
-        if ((rc = db->d8.ensure((size_t)KN * nchunks * ntiles * 4 * NT * KC))) return rc;
-        CK(cudaMemsetAsync(db->d8.p, 0, db->d8.bytes, s));
-        PackSrc ps{db->data.as<u32>(), (size_t)db->d0 * KN, 0, 1, (size_t)KN};
-        if ((rc = pack_planes(ps, (int)db->d1, (int)db->d0, NT, ntiles, nchunks, KC, db->d8.as<uint8_t>(), KN, s)))
+      r.PST = (!m64 && r.NT == 64)                               ? (pst_env == 2 ? 2 : 4)
+              : (pst_env == 2 || pst_env == 4 || pst_env == 8) ? pst_env
+              : m64                                            ? (r.NT == 64 ? 4 : 8)
+                                                               : 4;
+      r.KC = m64 ? 64 : 32;
+      r.nchunks = ((int)db->d0 + r.KC - 1) / r.KC;
+      r.ntiles = ((int)db->d1 + r.NT - 1) / r.NT;
+    }
+    // A8[p][c][mt][plane][g][row RA][16]
+    const size_t blk = (size_t)4 * r.RA * r.KC;
+    r.a8.base = nullptr;
+    r.a8.s_mt = blk;
+    r.a8.s_c = blk * r.mtiles;
+    r.a8.s_p = r.a8.s_c * r.nchunks;
+    r.a8.s_pl = (size_t)r.RA * r.KC;
+    r.a8.s_g = (size_t)r.RA * 16;
+    r.a8.G = r.KC / 16;
+    r.a8.RA = r.RA;
+    r.a8_bytes = r.a8.s_p * KN;
+    return r;
+  }
+
+  // DB byte planes D8[p][c][nt][plane][g][NT][16] in the plan's (NT, KC), packed once per layout
+  static int ensure_d8(gpir_ctx* c, gpir_db* db, const RsPlan& r, cudaStream_t s) {
+    const int KN = K * N;
+    if (db->d8_nt == r.NT && db->d8_kc == r.KC) return 0;
+    int rc;
+    if ((rc = db->d8.ensure((size_t)KN * r.nchunks * r.ntiles * 4 * r.NT * r.KC))) return rc;
+    CK(cudaMemsetAsync(db->d8.p, 0, db->d8.bytes, s));
+    PackSrc ps{db->data.as<u32>(), (size_t)db->d0 * KN, 0, 1, (size_t)KN};
+    if ((rc = pack_planes(ps, (int)db->d1, (int)db->d0, r.NT, r.ntiles, r.nchunks, r.KC, db->d8.as<uint8_t>(), KN, s)))
+      return rc;
+    db->d8_nt = r.NT;
+    db->d8_kc = r.KC;
+    // recorded graphs bake in the old byte-plane layout (the buffer may not have
+    // been reallocated): retire them like any reallocation
+    ++g_alloc_gen;
+    return 0;
+  }
+
+  static int set_smem_attr(gpir_ctx* c, const void* kern, size_t smem) {
+    // the attribute is set once per (device, kernel, size): no API calls inside a graph capture
+    static std::mutex mu;
+    static std::vector<std::tuple<int, const void*, size_t>> smem_set;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& ks : smem_set)
+      if (std::get<0>(ks) == c->device && std::get<1>(ks) == kern && std::get<2>(ks) >= smem) return 0;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set.emplace_back(c->device, kern, smem);
+    return 0;
+  }
+
+  // RowSel: tensor-core path (byte-plane u8 GEMMs, rowsel_tc.cuh) when the
+  // shape allows, else the CUDA-core kernel.  ev_mid (if non-null) is
+  // recorded between operand packing and the GEMM.  a8_ready: the A operand
+  // was already written in the plan's layout into ws_a8 (fused into the last
+  // ExpandQuery stage).  want_il: the caller takes the ColTor pair-interleaved
+  // output (kernels.cuh PAIRS_IL); *il_out reports whether it was produced.
+  static int rowsel(gpir_ctx* c, const u32* leaves, size_t a_b_words, int B, gpir_db* db, u32* sel,
+                    cudaStream_t s, uint32_t* launches, cudaEvent_t ev_mid = nullptr, const RsPlan* plan = nullptr,
+                    bool a8_ready = false, bool want_il = false, bool* il_out = nullptr) {
+    const int KN = K * N;
+    int rc;
+    if (il_out) *il_out = false;
+    const RsPlan r = plan ? *plan : rs_plan(c, B, db);
+    if (r.kind >= 1) {
+      if ((rc = ensure_d8(c, db, r, s))) return rc;
+      if ((rc = c->ws_a8.ensure(r.a8_bytes))) return rc;
+      if (!a8_ready) {
+        PackSrc pa{leaves, a_b_words, (size_t)KN, 2, 2 * (size_t)KN};
+        if ((rc = pack_planes(pa, r.M, (int)db->d0, r.RA, r.mtiles, r.nchunks, r.KC, c->ws_a8.as<uint8_t>(), KN, s)))
           return rc;
-        CKL();
-        db->d8_nt = NT;
-        db->d8_kc = KC;
+        ++*launches;
       }
-      if ((rc = c->ws_a8.ensure((size_t)KN * nchunks * mtiles * 4 * RA * KC))) return rc;
-      PackSrc pa{leaves, a_b_words, (size_t)KN, 2, 2 * (size_t)KN};
-      if ((rc = pack_planes(pa, M, (int)db->d0, RA, mtiles, nchunks, KC, c->ws_a8.as<uint8_t>(), KN, s))) return rc;
       if (ev_mid) CK(cudaEventRecord(ev_mid, s));
+    }
+    if (r.kind == 2) {
+      TkArgs ta;
+      ta.A8 = c->ws_a8.as<uint8_t>();
+      ta.D8 = db->d8.as<uint8_t>();
+      ta.out = sel;
+      ta.M = r.M;
+      ta.mtiles = r.mtiles;
+      ta.d1 = (int)db->d1;
+      ta.ntiles = r.ntiles;
+      ta.KN = KN;
+      ta.logn = LOGN;
+      ta.KC = r.KC;
+      ta.units = KN * r.mtiles;
+      ta.out_il = (want_il && db->d1 >= 2) ? 1 : 0;
+      const size_t slot = (size_t)128 * r.KC;
+      const size_t fixed = (2 * TK_MAX_SLOTS + 16) * 8 + 16;
+      ta.slots = std::min<int>(TK_MAX_SLOTS, (int)((226u * 1024u - fixed) / slot));
+      const size_t smem = (size_t)ta.slots * slot + fixed;
+      if ((rc = set_smem_attr(c, (const void*)k_rowsel_tk, smem))) return rc;
+      const int grid = std::min(ta.units, c->num_sms);
+      k_rowsel_tk<<<grid, TC_THREADS, smem, s>>>(ta, c->tb);
+      CKL();
+      ++*launches;
+      if (il_out) *il_out = ta.out_il != 0;
+      return 0;
+    }
+    if (r.kind == 1) {
+      const bool m64 = r.RA <= 64;
+      static const int ord_env = getenv("GPIR_TC_ORDER") ? atoi(getenv("GPIR_TC_ORDER")) : -1;
+      const int NT = r.NT, PST = r.PST, KC = r.KC, RA = r.RA;
       TcArgs ta;
       ta.A8 = c->ws_a8.as<uint8_t>();
       ta.D8 = db->d8.as<uint8_t>();
       ta.out = sel;
-      ta.M = M;
+      ta.M = r.M;
       ta.RA = RA;
-      ta.mtiles = mtiles;
+      ta.mtiles = r.mtiles;
       ta.d1 = (int)db->d1;
-      ta.ntiles = ntiles;
-      ta.nchunks = nchunks;
+      ta.ntiles = r.ntiles;
+      ta.nchunks = r.nchunks;
       ta.KN = KN;
       ta.logn = LOGN;
-      ta.items = KN * ntiles * mtiles;
+      ta.items = KN * r.ntiles * r.mtiles;
       ta.nt_outer = ord_env >= 0 ? ord_env : 0;
       const uint32_t stage_bytes = ((4u * RA * KC + 4u * NT * KC) + 127u) & ~127u;
       const size_t outbuf = (size_t)PST * RA * (NT + 1) * 4;
@@ -679,18 +802,7 @@ struct Engine {
                                   : (PST == 2   ? k_rowsel_tc<32, false, 2, 32>
                                      : PST == 4 ? k_rowsel_tc<32, false, 4, 32>
                                                 : k_rowsel_tc<32, false, 8, 32>));
-      {  // the attribute is set once per (device, kernel, size): no API calls inside a graph capture
-        static std::mutex mu;
-        static std::vector<std::tuple<int, const void*, size_t>> smem_set;
-        std::lock_guard<std::mutex> lk(mu);
-        bool have = false;
-        for (auto& ks : smem_set)
-          have |= (std::get<0>(ks) == c->device && std::get<1>(ks) == (const void*)kern && std::get<2>(ks) >= smem);
-        if (!have) {
-          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          smem_set.emplace_back(c->device, (const void*)kern, smem);
-        }
-      }
+      if ((rc = set_smem_attr(c, (const void*)kern, smem))) return rc;
       kern<<<grid, TC_THREADS, smem, s>>>(ta, c->tb);
       CKL();
       if (prof_on) {
@@ -704,7 +816,7 @@ struct Engine {
                 sum[0], sum[1], sum[2], sum[3], sum[4]);
         profbuf.release();
       }
-      *launches += 2;
+      ++*launches;
       return 0;
     }
     const int mt = (2 * B + RS_MT - 1) / RS_MT, nt = ((int)db->d1 + RS_NT - 1) / RS_NT;
@@ -765,16 +877,24 @@ struct Engine {
   }
 
   // expansion of B brv queries (in ws_state0 as (B,1)) -> leaves pointer (B, total)
+  // a8f: the RowSel A-operand layout to fuse into the last stage (or null);
+  // *fused reports whether the last stage wrote it (operation-level last stage,
+  // d0 % 16 == 0, d0 <= its node count per query)
   static int expand_all(gpir_ctx* c, int B, uint32_t total, const uint8_t* eq_modes, uint32_t n_eq,
-                        const int* kslot, u32** leaves_out, cudaStream_t s, uint32_t* launches) {
+                        const int* kslot, u32** leaves_out, cudaStream_t s, uint32_t* launches,
+                        const A8Desc* a8f = nullptr, int d0 = 0, bool* fused = nullptr) {
     const uint32_t stages = stages_of(total);
     u32* cur = c->ws_state0.as<u32>();
     u32* nxt = c->ws_state1.as<u32>();
+    if (fused) *fused = false;
     for (uint32_t t = 0; t < stages; ++t) {
       const int C = (int)std::min<uint32_t>(1u << t, total);
       const int Cout = (int)std::min<uint32_t>(2u << t, total);
       const int mode = (eq_modes && t < n_eq) ? eq_modes[t] : default_mode(B * C);
-      int rc = expand_stage(c, cur, B, C, nxt, Cout, (int)t, evk_rows(c, (int)t, kslot), mode, s, launches);
+      const bool fuse = a8f && t + 1 == stages && mode == 0 && d0 > 0 && d0 % 16 == 0 && d0 <= C && C % 16 == 0;
+      int rc = expand_stage(c, cur, B, C, nxt, Cout, (int)t, evk_rows(c, (int)t, kslot), mode, s, launches,
+                            fuse ? a8f : nullptr, d0);
+      if (fuse && fused) *fused = true;
       if (rc) return rc;
       g_sprof.mark(s, "eq" + std::to_string(t) + " " + "oFSH"[mode & 3], 0, (int)t, mode, (uint32_t)(B * C));
       std::swap(cur, nxt);
@@ -813,9 +933,10 @@ struct Engine {
   // Runs expansion over (d0, d1_tree), RGSW assembly for all log2(d1_tree)
   // bits, RowSel on db, and the low log2(db->d1) ColTor stages; returns the
   // pointer to the (B, 1) brv result and the leaves / a-rows for the caller.
+  // keep_rows: the caller reads the u32 row leaves afterwards (no fused A-operand write)
   static int pipeline(gpir_ctx* c, gpir_db* db, uint32_t d1_tree, int B, const uint8_t* eq_modes, uint32_t n_eq,
                       const uint8_t* ct_modes, uint32_t n_ct, const int* kslot, cudaStream_t s, gpir_stats* st,
-                      u32** result, u32** leaves_out) {
+                      u32** result, u32** leaves_out, bool keep_rows = false) {
     const uint32_t d0 = db->d0, d1 = db->d1;
     const uint32_t total = leaves_of(d0, d1_tree, ELL);
     const uint32_t bits_tree = ilog2(d1_tree), bits = ilog2(d1);
@@ -825,7 +946,19 @@ struct Engine {
     g_sprof.begin(c->stage_timing != 0);
     g_sprof.mark(s, "start");
     u32* leaves = nullptr;
-    if ((rc = expand_all(c, B, total, eq_modes, n_eq, kslot, &leaves, s, &launches))) return rc;
+    // RowSel plan first: its A-operand layout is written by the last ExpandQuery stage
+    RsPlan rp = rs_plan(c, B, db);
+    A8Desc a8f = rp.a8;
+    bool fused = false;
+    static const bool fuse_env = !getenv("GPIR_FUSE_A8") || atoi(getenv("GPIR_FUSE_A8")) != 0;
+    const bool fuse_ok = rp.kind >= 1 && fuse_env && !keep_rows;
+    if (fuse_ok) {
+      if ((rc = c->ws_a8.ensure(rp.a8_bytes))) return rc;
+      a8f.base = c->ws_a8.as<uint8_t>();
+    }
+    if ((rc = expand_all(c, B, total, eq_modes, n_eq, kslot, &leaves, s, &launches, fuse_ok ? &a8f : nullptr,
+                         (int)d0, &fused)))
+      return rc;
     if (st) CK(cudaEventRecord(c->ev[2], s));
     // RGSW assembly (src/protocol.py:383-409): a-rows = col_cts ⊡ RGSW(s)
     if (bits_tree > 0) {
@@ -838,8 +971,9 @@ struct Engine {
     }
     if (st) CK(cudaEventRecord(c->ev[3], s));
     g_sprof.mark(s, "rgsw", 1, 0, xp_default((size_t)B * bits_tree * ELL), (uint32_t)(B * bits_tree * ELL));
+    bool il = false;
     if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches,
-                     st ? c->ev[11] : nullptr)))
+                     st ? c->ev[11] : nullptr, &rp, fused, bits > 0, &il)))
       return rc;
     if (st) CK(cudaEventRecord(c->ev[4], s));
     g_sprof.mark(s, "rowsel+pack", 2, 0, 0, (uint32_t)B);
@@ -854,7 +988,9 @@ struct Engine {
       const RowsDesc r = coltor_rows(c, bits, j);
       const int mode = (ct_modes && j < n_ct) ? ct_modes[j] : xp_default((size_t)B * C / 2);
       u32* dst = bufs[j & 1];
-      if ((rc = ext_product(c, cur, (size_t)C, B, C / 2, 1, dst, (size_t)C / 2, r, mode, s, &launches))) return rc;
+      if ((rc = ext_product(c, cur, (size_t)C, B, C / 2, (j == 0 && il) ? PAIRS_IL : 1, dst, (size_t)C / 2, r, mode, s,
+                            &launches)))
+        return rc;
       g_sprof.mark(s, "coltor" + std::to_string(j) + " " + "oFSH"[mode & 3], 3, (int)j, mode, (uint32_t)(B * C / 2));
       cur = dst;
     }
@@ -1443,6 +1579,7 @@ gpir_ctx* gpir_ctx_create(int device, uint32_t n, uint32_t k, const uint32_t* q,
   if (const char* ge = getenv("GPIR_GRAPH")) c->use_graph = atoi(ge);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   for (auto& ev : c->ev) cudaEventCreate(&ev);
+  cudaEventCreateWithFlags(&c->ev_legacy, cudaEventDisableTiming);
   return c;
 }
 
@@ -1455,6 +1592,7 @@ void gpir_ctx_destroy(gpir_ctx* c) {
                     &c->ws_dn, &c->ws_io0, &c->ws_io1, &c->ws_a8})
     b->release();
   for (auto& ev : c->ev) cudaEventDestroy(ev);
+  if (c->ev_legacy) cudaEventDestroy(c->ev_legacy);
   for (auto& g : c->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   cudaStreamDestroy(c->stream);
@@ -1851,7 +1989,7 @@ int gpir_answer_batch_dev(gpir_ctx* c, const gpir_db* db, const uint32_t* d_quer
   if (B == 0) return 0;
   std::lock_guard<std::mutex> lk(c->mu);
   CK(cudaSetDevice(c->device));
-  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  cudaStream_t s = pick_stream(c, stream);
   if (stats) memset(stats, 0, sizeof(*stats));
   int rc = answer_dev_dispatch(c, db, d_queries, key_slots, B, eq_modes, n_eq, ct_modes, n_ct, d_responses, s, stats);
   if (rc) return rc;
@@ -1924,7 +2062,7 @@ int gpir_shard_answer(gpir_ctx* c, const gpir_db* db, uint32_t d1_total, const u
   if (!c || !db || !d_queries || !key_slots || !d_partials) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
   CK(cudaSetDevice(c->device));
-  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  cudaStream_t s = pick_stream(c, stream);
   if (stats) memset(stats, 0, sizeof(*stats));
   int rc;
   switch (c->logn * 10000 + c->k * 100 + c->ell) {
@@ -1947,7 +2085,7 @@ int gpir_sharded_expand(gpir_ctx* c, uint32_t d0, uint32_t d1, const uint32_t* d
     FAIL(GPIR_INVALID_ARGUMENT, "invalid sharded expansion input");
   std::lock_guard<std::mutex> lk(c->mu);
   CK(cudaSetDevice(c->device));
-  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  cudaStream_t s = pick_stream(c, stream);
   int rc;
   switch (c->logn * 10000 + c->k * 100 + c->ell) {
     GPIR_COMBOS(DISPATCH_CASE_SHX)
@@ -1964,7 +2102,7 @@ int gpir_sharded_rowsel(gpir_ctx* c, const gpir_db* db, const uint32_t* d_rows, 
   if (!c || !db || !d_rows || !d_partial || !B) FAIL(GPIR_INVALID_ARGUMENT, "invalid sharded rowsel input");
   std::lock_guard<std::mutex> lk(c->mu);
   CK(cudaSetDevice(c->device));
-  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  cudaStream_t s = pick_stream(c, stream);
   int rc;
   uint32_t launches = 0;
   gpir_db* mdb = const_cast<gpir_db*>(db);
@@ -1987,7 +2125,7 @@ int gpir_sharded_rgsw(gpir_ctx* c, uint32_t bit_lo, uint32_t bit_hi, uint32_t* d
   if (!c || !d_rgsw) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
   CK(cudaSetDevice(c->device));
-  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  cudaStream_t s = pick_stream(c, stream);
   int rc;
   switch (c->logn * 10000 + c->k * 100 + c->ell) {
     GPIR_COMBOS(DISPATCH_CASE_SHR)
@@ -2003,7 +2141,7 @@ int gpir_layout_convert(gpir_ctx* c, const uint32_t* d_in, uint32_t* d_out, uint
   if (!c || !d_in || !d_out) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
   CK(cudaSetDevice(c->device));
-  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  cudaStream_t s = pick_stream(c, stream);
   int rc = bitrev_rows(c, d_in, d_out, (size_t)polys * c->k, s);
   if (rc) return rc;
   if (!stream) CK(cudaStreamSynchronize(s));
@@ -2018,7 +2156,7 @@ int gpir_sharded_coltor(gpir_ctx* c, uint32_t* d_sums, uint32_t B, uint32_t* d_o
   if (!c || !d_sums || !d_out || !B) FAIL(GPIR_INVALID_ARGUMENT, "invalid sharded coltor input");
   std::lock_guard<std::mutex> lk(c->mu);
   CK(cudaSetDevice(c->device));
-  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  cudaStream_t s = pick_stream(c, stream);
   int rc;
   switch (c->logn * 10000 + c->k * 100 + c->ell) {
     GPIR_COMBOS(DISPATCH_CASE_SHC)
@@ -2039,7 +2177,7 @@ int gpir_coltor_dev(gpir_ctx* c, const uint32_t* d_cts, uint32_t B, uint32_t C, 
   if (!c || !d_cts || !d_out || !C || (C & (C - 1))) FAIL(GPIR_INVALID_ARGUMENT, "invalid tournament input");
   std::lock_guard<std::mutex> lk(c->mu);
   CK(cudaSetDevice(c->device));
-  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  cudaStream_t s = pick_stream(c, stream);
   int rc;
   switch (c->logn * 10000 + c->k * 100 + c->ell) {
     GPIR_COMBOS(DISPATCH_CASE_CT)

@@ -44,6 +44,62 @@ __device__ __forceinline__ void st16(u32* p, const u32 (&x)[16]) {
   for (int c = 0; c < 4; ++c) v[c] = make_uint4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
 }
 
+// ColTor pair input (coltor_stage, src/planner.py:457-463).  pairs == 1: the even
+// ct at src and the odd one at src + CT (the standard layout); pairs == 2: the
+// pair interleaved word by word -- element e of the even ct at src[2e], of the
+// odd one at src[2e + 1] -- which is what the tensor-core RowSel epilogue
+// writes (one 8-byte store per pair and slot, rowsel_tc.cuh k_rowsel_tk).
+constexpr int PAIRS_IL = 2;
+__device__ __forceinline__ u32 pair_even1(const u32* __restrict__ src, size_t off, int pairs) {
+  return pairs == PAIRS_IL ? __ldg(src + 2 * off) : __ldg(src + off);
+}
+__device__ __forceinline__ u32 pair_diff1(const u32* __restrict__ src, size_t off, int pairs, size_t CT, u32 q) {
+  if (pairs == PAIRS_IL) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(src + 2 * off));
+    return mod_sub(v.y, v.x, q);
+  }
+  return mod_sub(__ldg(src + CT + off), __ldg(src + off), q);
+}
+// 4 consecutive elements of the even and the odd ct (off multiple of 4)
+__device__ __forceinline__ void pair_ld4(const u32* __restrict__ src, size_t off, int pairs, size_t CT, uint4& ev,
+                                         uint4& od) {
+  if (pairs == PAIRS_IL) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(src + 2 * off));
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(src + 2 * off) + 1);
+    ev = make_uint4(a.x, a.z, b.x, b.z);
+    od = make_uint4(a.y, a.w, b.y, b.w);
+  } else {
+    ev = __ldg(reinterpret_cast<const uint4*>(src + off));
+    od = __ldg(reinterpret_cast<const uint4*>(src + CT + off));
+  }
+}
+__device__ __forceinline__ uint4 pair_even4(const u32* __restrict__ src, size_t off, int pairs) {
+  if (pairs == PAIRS_IL) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(src + 2 * off));
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(src + 2 * off) + 1);
+    return make_uint4(a.x, a.z, b.x, b.z);
+  }
+  return __ldg(reinterpret_cast<const uint4*>(src + off));
+}
+// odd - even over 16 consecutive elements
+__device__ __forceinline__ void pair_diff16(const u32* __restrict__ src, size_t off, int pairs, size_t CT, u32 q,
+                                            u32 (&x)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint4 e, o;
+    pair_ld4(src, off + 4 * c, pairs, CT, e, o);
+    x[4 * c] = mod_sub(o.x, e.x, q), x[4 * c + 1] = mod_sub(o.y, e.y, q);
+    x[4 * c + 2] = mod_sub(o.z, e.z, q), x[4 * c + 3] = mod_sub(o.w, e.w, q);
+  }
+}
+__device__ __forceinline__ void pair_even16(const u32* __restrict__ src, size_t off, int pairs, u32 (&x)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 e = pair_even4(src, off + 4 * c, pairs);
+    x[4 * c] = e.x, x[4 * c + 1] = e.y, x[4 * c + 2] = e.z, x[4 * c + 3] = e.w;
+  }
+}
+
 // acc{0,1}[r] += x[r] * row{a,b}[r] over 16 consecutive brv slots, 4 at a time
 __device__ __forceinline__ void mac16(const u32 (&x)[16], const u32* __restrict__ ra, const u32* __restrict__ rb,
                                       Acc (&acc0)[16], Acc (&acc1)[16]) {
@@ -96,8 +152,11 @@ __device__ __forceinline__ void mont_mac16(const u32 (&x)[16], const Key16& ka, 
 // carry-rule digits in closed form: with T = mag + sum_{j<ell-1} (z/2-1) z^j,
 // digit j < ell-1 is bits [jz, jz+z) of T minus (z/2 - 1) and the last digit
 // is T >> (ell-1) z (the rule keeps raw == z/2 positive, so the balanced
-// digits lie in [-z/2+1, z/2]; checked exhaustively on the boundary patterns
-// against the reference loop in tests/test_oracle.py).
+// digits lie in [-z/2+1, z/2]; pinned against the reference's DigitExtractor
+// on crafted boundary coefficients -- raw digit z/2 and z/2+1 at every position,
+// carry chains through all ell digits, +-(Q-1)/2 -- by
+// tests/test_gpu_parity.py::test_digits_boundary_vectors, vectors from
+// tools/make_digit_golden.py).
 struct W4 {
   u32 w0, w1, w2, w3;
 };
@@ -420,7 +479,6 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
   const int b = blockIdx.x / M_per_b, m = blockIdx.x % M_per_b;
   const size_t CT = 2 * (size_t)K * N;
   const u32* src = pairs ? in + (b * in_b + 2 * (size_t)m) * CT : in + (b * in_b + (size_t)m) * CT;
-  const u32* odd = src + CT;
   u32* dst = out + (b * out_b + (size_t)m) * CT;
   const int i0 = tid << 4;
 
@@ -433,13 +491,10 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
       ntt_inv<LOGN>(
           ns, tb.inv + (size_t)i * N, tc.i[i], Mi,
           [&](int j0, u32(&x)[16]) {
-            ld16(src + off + j0, x);
-            if (pairs) {
-              u32 o[16];
-              ld16(odd + off + j0, o);
-#pragma unroll
-              for (int r = 0; r < 16; ++r) x[r] = mod_sub(o[r], x[r], Mi.q);
-            }
+            if (pairs)
+              pair_diff16(src, off + j0, pairs, CT, Mi.q, x);
+            else
+              ld16(src + off + j0, x);
           },
           [&](int, int r, u32 v) { priv[pv<T>(i, r)] = (int)v; });
     }
@@ -463,13 +518,10 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
         if (j == ELL - 1) {  // folded top digit: MAC this component of the input directly
           const size_t off = (size_t)(comp * K + i) * N + i0;
           u32 x[16];
-          ld16(src + off, x);
-          if (pairs) {
-            u32 o[16];
-            ld16(odd + off, o);
-#pragma unroll
-            for (int r = 0; r < 16; ++r) x[r] = mod_sub(o[r], x[r], q);
-          }
+          if (pairs)
+            pair_diff16(src, off, pairs, CT, q, x);
+          else
+            ld16(src + off, x);
           mont_mac16(x, ka, kb, acc0, acc1, q, qinv);
           break;
         }
@@ -495,8 +547,8 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, FUSED_MINB)
           sb[r] = mod_add(sb[r], pb[r], q);
         }
         if (pairs) {
-          ld16(src + (size_t)i * N + i0, pa);
-          ld16(src + (size_t)(K + i) * N + i0, pb);
+          pair_even16(src, (size_t)i * N + i0, pairs, pa);
+          pair_even16(src, (size_t)(K + i) * N + i0, pairs, pb);
 #pragma unroll
           for (int r = 0; r < 16; ++r) {
             sa[r] = mod_add(sa[r], pa[r], q);
@@ -571,13 +623,10 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
   ntt_inv<LOGN>(
       ns, tb.inv + (size_t)i * N, tc.i[i], tb.mod[i],
       [&](int j0, u32(&x)[16]) {
-        ld16(src + off + j0, x);
-        if (pairs) {
-          u32 o[16];
-          ld16(src + CT + off + j0, o);
-#pragma unroll
-          for (int r = 0; r < 16; ++r) x[r] = mod_sub(o[r], x[r], q);
-        }
+        if (pairs)
+          pair_diff16(src, off + j0, pairs, CT, q, x);
+        else
+          ld16(src + off + j0, x);
       },
       [&](int j, int, u32 v) { dst[j] = v; });
 }
@@ -830,6 +879,106 @@ __global__ void __launch_bounds__(256) k_op_eq_mac_nb4(const u32* __restrict__ s
   }
 }
 
+// Byte-plane layout of the tensor-core RowSel A operand (rowsel_tc.cuh): the
+// 16-byte K group kg (depth k = 16 kg ..) of row m at slot p, plane pl lives at
+// p s_p + (kg / G) s_c + (m / RA) s_mt + pl s_pl + (kg % G) s_g + (m % RA) 16.
+// Rows 2b and 2b + 1 (the a and b components of query b) are adjacent 16-byte
+// pieces of one core matrix, so the two components form one 32-byte sector.
+struct A8Desc {
+  uint8_t* base;
+  size_t s_p, s_c, s_mt, s_pl, s_g;
+  int G, RA;
+  __device__ __forceinline__ uint8_t* at(int p, int m, int kg, int pl) const {
+    return base + (size_t)p * s_p + (size_t)(kg / G) * s_c + (size_t)(m / RA) * s_mt + (size_t)pl * s_pl +
+           (size_t)(kg % G) * s_g + (size_t)(m % RA) * 16;
+  }
+};
+
+// (4a-iv) the LAST ExpandQuery stage's MAC + combine with the RowSel operand
+// pack fused in (_expanded_to_in0 + transpose_ct_tensor, src/protocol.py:426-441,
+// src/layout.py:156-178): 16 consecutive nodes of one query per thread, one
+// slot.  The `c + s` outputs of nodes c < d0 are the row ciphertexts; instead
+// of their u32 words the thread writes their byte planes -- 16 nodes = one
+// 16-byte K group per (row, plane) -- straight into the A operand (a8), so
+// RowSel needs no separate packing pass over the row leaves.  Requires
+// node0 % 16 == 0, C % 16 == 0, d0 % 16 == 0 and d0 <= C (rows only among the
+// first outputs); all other outputs are written as usual.
+template <int LOGN, int K, int ELL>
+__global__ void __launch_bounds__(256) k_op_eq_mac_a8(const u32* __restrict__ state, int C, int node0, int nodes,
+                                                      const u32* __restrict__ dn, RowsDesc ksk, u32 k_aut,
+                                                      const uint2* __restrict__ mono, u32* __restrict__ out, int Cout,
+                                                      Tables tb, A8Desc a8, int d0) {
+  constexpr int N = 1 << LOGN;
+  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t groups = (size_t)nodes / 16;
+  if (g >= groups * K * N) return;
+  const int pos = (int)(g & (N - 1));
+  const int i = (int)((g >> LOGN) % K);
+  const int nd0 = (int)(g / ((size_t)K * N)) * 16;
+  const size_t CT = 2 * (size_t)K * N;
+  const Modulus M = tb.mod[i];
+  const u32 q = M.q;
+  const u32 src_pos = aut_src(pos, k_aut, LOGN);
+  const uint2 w = __ldg(&mono[(size_t)i * N + pos]);
+  const int gn0 = node0 + nd0;
+  const int b = gn0 / C, c0 = gn0 % C;
+  u32 ka[ELL], kb[ELL];
+#pragma unroll
+  for (int j = 0; j < ELL; ++j) {
+    const u32* ra = ksk.row(b, j, ELL, CT) + (size_t)i * N + pos;
+    ka[j] = __ldg(ra);
+    kb[j] = __ldg(ra + (size_t)K * N);
+  }
+  const bool rows = c0 < d0;
+  u32 pa[4][4], pb[4][4];  // [plane][word]: byte u of the 16-byte K group = node c0 + u
+#pragma unroll
+  for (int pl = 0; pl < 4; ++pl)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) pa[pl][v] = pb[pl][v] = 0;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int nd = nd0 + u;
+    const int c = c0 + u;
+    const u32* st = state + (size_t)(gn0 + u) * CT;
+    u64 a0 = 0, a1 = 0;
+#pragma unroll
+    for (int j = 0; j < ELL; ++j) {  // digit ELL-1 is folded: its term is tau(a) itself
+      const u32 d = j < ELL - 1 ? __ldg(dn + (((size_t)nd * ELL + j) * K + i) * N + pos) : __ldg(st + (size_t)i * N + src_pos);
+      a0 += (u64)d * ka[j];
+      a1 += (u64)d * kb[j];
+    }
+    const u32 ca = __ldg(st + (size_t)i * N + pos), cb = __ldg(st + (size_t)(K + i) * N + pos);
+    const u32 sa = reduce_u64(a0, M);
+    const u32 sb = mod_add(reduce_u64(a1, M), __ldg(st + (size_t)(K + i) * N + src_pos), q);
+    const u32 xa = mod_add(ca, sa, q), xb = mod_add(cb, sb, q);
+    if (rows) {
+#pragma unroll
+      for (int pl = 0; pl < 4; ++pl) {
+        pa[pl][u >> 2] |= ((xa >> (8 * pl)) & 0xffu) << (8 * (u & 3));
+        pb[pl][u >> 2] |= ((xb >> (8 * pl)) & 0xffu) << (8 * (u & 3));
+      }
+    } else {
+      u32* o0 = out + ((size_t)b * Cout + c) * CT;
+      o0[(size_t)i * N + pos] = xa;
+      o0[(size_t)(K + i) * N + pos] = xb;
+    }
+    if (c + C < Cout) {
+      u32* o1 = out + ((size_t)b * Cout + c + C) * CT;
+      o1[(size_t)i * N + pos] = csub(mul_shoup(mod_sub(ca, sa, q), w.x, w.y, q), q);
+      o1[(size_t)(K + i) * N + pos] = csub(mul_shoup(mod_sub(cb, sb, q), w.x, w.y, q), q);
+    }
+  }
+  if (rows) {
+    const int p = i * N + pos, kg = c0 >> 4;
+#pragma unroll
+    for (int pl = 0; pl < 4; ++pl) {
+      uint4* d = reinterpret_cast<uint4*>(a8.at(p, 2 * b, kg, pl));  // rows 2b, 2b + 1: one 32-byte sector
+      d[0] = make_uint4(pa[pl][0], pa[pl][1], pa[pl][2], pa[pl][3]);
+      d[1] = make_uint4(pb[pl][0], pb[pl][1], pb[pl][2], pb[pl][3]);
+    }
+  }
+}
+
 // (4b) external-product MAC (+ ColTor combine); one thread per (ct, limb, slot).
 template <int LOGN, int K, int ELL>
 __global__ void k_op_xp_mac(const u32* __restrict__ in, size_t in_b, int M_per_b, int m0, int cts, int pairs,
@@ -856,8 +1005,7 @@ __global__ void k_op_xp_mac(const u32* __restrict__ in, size_t in_b, int M_per_b
         d = __ldg(dn + ((((size_t)ct * 2 + comp) * ELL + j) * K + i) * N + pos);
       } else {  // folded top digit: this component of the input (or odd - even)
         const size_t off = (size_t)(comp * K + i) * N + pos;
-        d = __ldg(src + off);
-        if (pairs) d = mod_sub(__ldg(src + CT + off), d, q);
+        d = pairs ? pair_diff1(src, off, pairs, CT, q) : __ldg(src + off);
       }
       const u32* ra = rows.row(b, comp * ELL + j, ELL, CT) + (size_t)i * N + pos;
       a0 += (u64)d * __ldg(ra);
@@ -867,8 +1015,8 @@ __global__ void k_op_xp_mac(const u32* __restrict__ in, size_t in_b, int M_per_b
   u32 sa = reduce_u64(a0, M), sb = reduce_u64(a1, M);
   if (pairs) {
     const u32* ev = in + (b * in_b + 2 * (size_t)m) * CT;
-    sa = mod_add(sa, __ldg(ev + (size_t)i * N + pos), q);
-    sb = mod_add(sb, __ldg(ev + (size_t)(K + i) * N + pos), q);
+    sa = mod_add(sa, pair_even1(ev, (size_t)i * N + pos, pairs), q);
+    sb = mod_add(sb, pair_even1(ev, (size_t)(K + i) * N + pos, pairs), q);
   }
   u32* d = out + (b * out_b + (size_t)m) * CT;
   d[(size_t)i * N + pos] = sa;
@@ -920,8 +1068,7 @@ __global__ void k_op_xp_mac_nb(const u32* __restrict__ in, size_t in_b, int M_pe
           d = __ldg(dn + ((((size_t)ct * 2 + comp) * ELL + j) * K + i) * N + pos);
         } else {  // folded top digit: this component of the input (or odd - even)
           const size_t off = (size_t)(comp * K + i) * N + pos;
-          d = __ldg(src + off);
-          if (pairs) d = mod_sub(__ldg(src + CT + off), d, q);
+          d = pairs ? pair_diff1(src, off, pairs, CT, q) : __ldg(src + off);
         }
         a0 += (u64)d * ka[comp * ELL + j];
         a1 += (u64)d * kb[comp * ELL + j];
@@ -930,8 +1077,8 @@ __global__ void k_op_xp_mac_nb(const u32* __restrict__ in, size_t in_b, int M_pe
     u32 sa = reduce_u64(a0, M), sb = reduce_u64(a1, M);
     if (pairs) {
       const u32* ev = in + (b * in_b + 2 * (size_t)m) * CT;
-      sa = mod_add(sa, __ldg(ev + (size_t)i * N + pos), q);
-      sb = mod_add(sb, __ldg(ev + (size_t)(K + i) * N + pos), q);
+      sa = mod_add(sa, pair_even1(ev, (size_t)i * N + pos, pairs), q);
+      sb = mod_add(sb, pair_even1(ev, (size_t)(K + i) * N + pos, pairs), q);
     }
     u32* d = out + (b * out_b + (size_t)m) * CT;
     d[(size_t)i * N + pos] = sa;
@@ -982,10 +1129,12 @@ __global__ void __launch_bounds__(256) k_op_xp_mac_nb4(const u32* __restrict__ i
           v = __ldg(reinterpret_cast<const uint4*>(dn + ((((size_t)ct * 2 + comp) * ELL + j) * K + i) * N + pos));
         } else {  // folded top digit: this component of the input (or odd - even)
           const size_t off = (size_t)(comp * K + i) * N + pos;
-          v = __ldg(reinterpret_cast<const uint4*>(src + off));
           if (pairs) {
-            const uint4 o = __ldg(reinterpret_cast<const uint4*>(src + CT + off));
+            uint4 o;
+            pair_ld4(src, off, pairs, CT, v, o);
             v = make_uint4(mod_sub(o.x, v.x, q), mod_sub(o.y, v.y, q), mod_sub(o.z, v.z, q), mod_sub(o.w, v.w, q));
+          } else {
+            v = __ldg(reinterpret_cast<const uint4*>(src + off));
           }
         }
         const uint4 kr = ka[comp * ELL + j], ks = kb[comp * ELL + j];
@@ -998,8 +1147,8 @@ __global__ void __launch_bounds__(256) k_op_xp_mac_nb4(const u32* __restrict__ i
     for (int r = 0; r < 4; ++r) sa[r] = reduce_u64(a0[r], M), sb[r] = reduce_u64(a1[r], M);
     if (pairs) {
       const u32* ev = in + (b * in_b + 2 * (size_t)m) * CT;
-      const uint4 ea = __ldg(reinterpret_cast<const uint4*>(ev + (size_t)i * N + pos));
-      const uint4 eb = __ldg(reinterpret_cast<const uint4*>(ev + (size_t)(K + i) * N + pos));
+      const uint4 ea = pair_even4(ev, (size_t)i * N + pos, pairs);
+      const uint4 eb = pair_even4(ev, (size_t)(K + i) * N + pos, pairs);
       sa[0] = mod_add(sa[0], ea.x, q), sa[1] = mod_add(sa[1], ea.y, q), sa[2] = mod_add(sa[2], ea.z, q),
       sa[3] = mod_add(sa[3], ea.w, q);
       sb[0] = mod_add(sb[0], eb.x, q), sb[1] = mod_add(sb[1], eb.y, q), sb[2] = mod_add(sb[2], eb.z, q),

@@ -528,3 +528,208 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
 }
 
 }  // namespace gpir
+
+namespace gpir {
+
+// ---------------------------------------------------------------------------
+// RowSel with the A operand resident in tensor memory (k_rowsel_tk): the
+// M = 128 row tiles (2B > 64) for d0 <= 256.
+//
+// Work unit = (p, 128-row tile).  The unit's A operand -- 128 rows x KC bytes x
+// 4 byte planes (KC = d0 rounded up to one 32-byte MMA K step) -- is copied
+// into TMEM once (tcgen05.cp, columns [0, KC)) and feeds the MMAs of every
+// 32-column DB tile of that p: A crosses L2 once per unit instead of once per
+// column tile (the r1 kernel re-read it d1/32 times, 6.7x the algorithmic
+// operand bytes at config 3), and per MMA only the 1 KiB B slice is read from
+// shared memory.  The 7 anti-diagonal s32 accumulators (32 columns each, TMEM
+// columns [256, 480)) are single-buffered but issued diagonal by diagonal with
+// one commit per diagonal: the epilogue drains diagonal u of tile t into u64
+// registers while the MMAs of diagonals u+1.. run, and tile t+1 only waits for
+// that drain before its own diagonal u.  The next unit's four A planes are
+// copied in just before the first diagonal that needs them (tcgen05.cp and
+// tcgen05.mma execute in issue order, and plane u was last read by the
+// previous tile's diagonal <= u + 3, dozens of MMAs earlier).
+//
+// One shared-memory ring of 128 * KC-byte slots carries both the A planes
+// (128 rows x KC) and the DB tiles (4 planes x 32 columns x KC), each one
+// cp.async.bulk: A8[p][mt][plane][KC/16][128][16], D8[p][nt][plane][KC/16][32][16]
+// (UMMA canonical K-major, no swizzle).
+//
+// Output: out_il = 1 writes the ColTor pair layout (the two cts of a ColTor
+// pair interleaved word by word, kernels.cuh PAIRS_IL): the thread of row
+// m = 2b + comp holds 16 columns = 8 pairs of one p and stores each pair as one
+// 8-byte word pair; out_il = 0 writes the standard (B, d1, 2, K*N) layout.
+constexpr int TK_NT = 32;
+constexpr int TK_ACC0 = 256;  // first accumulator column
+constexpr int TK_MAX_SLOTS = 8;
+
+struct TkArgs {
+  const uint8_t* A8;
+  const uint8_t* D8;
+  u32* out;
+  int M;       // 2B
+  int mtiles;  // 128-row tiles
+  int d1, ntiles, KN, logn;
+  int KC;      // padded K bytes per plane (multiple of 32, <= 256)
+  int units;   // KN * mtiles
+  int slots;   // ring depth
+  int out_il;
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb) {
+  extern __shared__ __align__(1024) uint8_t tk_smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t slot_bytes = 128u * (uint32_t)a.KC;
+  const int NS = a.slots;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tk_smem + (size_t)NS * slot_bytes);
+  uint64_t* empty = full + TK_MAX_SLOTS;
+  uint64_t* dfull = empty + TK_MAX_SLOTS;
+  uint64_t* dempty = dfull + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 8);
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int u = 0; u < 7; ++u) {
+      mbar_init(&dfull[u], 1);
+      mbar_init(&dempty[u], TC_EPI_WARPS);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const int kst = a.KC >> 5;  // MMA K steps (32 bytes each)
+
+  if (warp == 0) {  // producer: per unit the 4 A planes, then the unit's DB tiles
+    const uint64_t pol_once = l2_policy_evict_first();
+    uint32_t item = 0;
+    for (int un = blockIdx.x; un < a.units; un += gridDim.x) {
+      const int p = un / a.mtiles, mt = un % a.mtiles;
+      for (int it = 0; it < 4 + a.ntiles; ++it, ++item) {
+        const uint32_t s = item % NS, ph = (item / NS) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        if (elect_one()) {
+          uint8_t* dst = tk_smem + (size_t)s * slot_bytes;
+          mbar_expect_tx(&full[s], slot_bytes);
+          if (it < 4)
+            bulk_g2s_hint(dst, a.A8 + ((size_t)(p * a.mtiles + mt) * 4 + it) * slot_bytes, slot_bytes, &full[s],
+                          pol_once);
+          else
+            bulk_g2s(dst, a.D8 + ((size_t)p * a.ntiles + (it - 4)) * slot_bytes, slot_bytes, &full[s]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {  // MMA issuer: one elected thread runs the whole schedule
+    constexpr uint32_t idesc = umma_idesc_u8(128, TK_NT);
+    if (elect_one()) {
+      uint32_t item = 0, tile = 0;
+      const uint32_t acol = (uint32_t)a.KC >> 2;  // TMEM columns per A plane
+      for (int un = blockIdx.x; un < a.units; un += gridDim.x) {
+        const uint32_t item_a = item;  // the unit's A planes: ring items item_a .. item_a + 3
+        item += 4;
+        for (int nt = 0; nt < a.ntiles; ++nt, ++item, ++tile) {
+          const uint32_t sb = item % NS, phb = (item / NS) & 1;
+          const uint32_t bbase = smem_u32(tk_smem + (size_t)sb * slot_bytes);
+          const uint32_t tph = (tile & 1) ^ 1;
+#pragma unroll 1
+          for (int u = 0; u < 7; ++u) {
+            if (nt == 0 && u < 4) {  // A plane u of this unit into TMEM columns [u * acol, (u + 1) * acol)
+              const uint32_t ia = item_a + u, sa = ia % NS;
+              mbar_wait(&full[sa], (ia / NS) & 1);
+              tc_fence_after();
+              const uint32_t abase = smem_u32(tk_smem + (size_t)sa * slot_bytes);
+              for (int ks = 0; ks < kst; ++ks)
+                tmem_cp_128x256b(tbase + u * acol + 8 * ks, umma_desc(abase + ks * 4096, 2048, 128));
+              umma_commit(&empty[sa]);  // slot free once the copies have landed
+            }
+            if (u == 0) {
+              mbar_wait(&full[sb], phb);
+              tc_fence_after();
+            }
+            mbar_wait(&dempty[u], tph);  // diagonal u of the previous tile drained
+            tc_fence_after();
+            const uint32_t dcol = tbase + TK_ACC0 + 32 * u;
+            const int sp0 = u > 3 ? u - 3 : 0, sp1 = u < 3 ? u : 3;
+            for (int sp = sp0; sp <= sp1; ++sp) {
+              const int tp = u - sp;
+              for (int ks = 0; ks < kst; ++ks)
+                umma_i8_ta(dcol, tbase + sp * acol + 8 * ks,
+                           umma_desc(bbase + tp * 32 * a.KC + ks * 1024, 512, 128), idesc,
+                           (sp == sp0 && ks == 0) ? 0u : 1u);
+            }
+            umma_commit(&dfull[u]);
+          }
+          umma_commit(&empty[sb]);  // DB tile free once every diagonal has read it
+        }
+      }
+    }
+    __syncwarp();
+  } else {  // epilogue warps 2..9: TMEM lanes 32 * (warp % 4) .., columns 16 * half ..
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const uint32_t lane_base = tbase + ((uint32_t)(quad * 32) << 16) + TK_ACC0 + 16 * half;
+    const int P2 = a.d1 >> 1;
+    uint32_t tile = 0;
+    for (int un = blockIdx.x; un < a.units; un += gridDim.x) {
+      const int p = un / a.mtiles, mt = un % a.mtiles;
+      const Modulus M = tb.mod[p >> a.logn];
+      const int m = mt * 128 + quad * 32 + lane;
+      const bool act = m < a.M;
+      const int b = m >> 1, comp = m & 1;
+      for (int nt = 0; nt < a.ntiles; ++nt, ++tile) {
+        u64 acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = 0;
+#pragma unroll
+        for (int u = 0; u < 7; ++u) {
+          mbar_wait(&dfull[u], tile & 1);
+          tc_fence_after();
+          uint32_t v[2][8];
+          tmem_ld8(lane_base + 32 * u, v[0]);
+          tmem_ld8(lane_base + 32 * u + 8, v[1]);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dempty[u]);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] += (u64)v[j >> 3][j & 7] << (8 * u);
+        }
+        if (act) {
+          const int n0 = nt * TK_NT + 16 * half;
+          if (a.out_il) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              const int pr = (n0 >> 1) + r;
+              if (pr < P2) {
+                u32* dst = a.out + ((((size_t)b * P2 + pr) * 2 + comp) * a.KN + p) * 2;
+                *reinterpret_cast<uint2*>(dst) = make_uint2(reduce_u64(acc[2 * r], M), reduce_u64(acc[2 * r + 1], M));
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int n = n0 + j;
+              if (n < a.d1) a.out[(((size_t)b * a.d1 + n) * 2 + comp) * a.KN + p] = reduce_u64(acc[j], M);
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+  }
+}
+
+}  // namespace gpir

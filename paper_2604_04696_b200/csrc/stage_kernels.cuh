@@ -92,13 +92,10 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
       ntt_inv<LOGN>(
           ns, tb.inv + (size_t)i * N, tc.i[i], Mi,
           [&](int j0, u32(&x)[16]) {
-            ld16(src + off + j0, x);
-            if (pairs) {
-              u32 o[16];
-              ld16(src + CT + off + j0, o);
-#pragma unroll
-              for (int r = 0; r < 16; ++r) x[r] = mod_sub(o[r], x[r], Mi.q);
-            }
+            if (pairs)
+              pair_diff16(src, off + j0, pairs, CT, Mi.q, x);
+            else
+              ld16(src + off + j0, x);
           },
           [&](int, int r, u32 v) { coef[i][r] = v; });
     }
@@ -268,13 +265,15 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, K2_MINB)
       ns, dig + (size_t)lc * 2 * ELL * N, 2, i, [&](int j) { return rows.row(b, j, ELL, CT); },
       [&](int comp, int h, u32(&x)[4]) {
         const size_t off = (size_t)(comp * K + i) * N + (tid << 4) + 4 * h;
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + off));
-        x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
         if (pairs) {
-          const uint4 o = __ldg(reinterpret_cast<const uint4*>(src + CT + off));
+          uint4 v, o;
+          pair_ld4(src, off, pairs, CT, v, o);
           const u32 q = tb.mod[i].q;
-          x[0] = mod_sub(o.x, x[0], q), x[1] = mod_sub(o.y, x[1], q), x[2] = mod_sub(o.z, x[2], q),
-          x[3] = mod_sub(o.w, x[3], q);
+          x[0] = mod_sub(o.x, v.x, q), x[1] = mod_sub(o.y, v.y, q), x[2] = mod_sub(o.z, v.z, q),
+          x[3] = mod_sub(o.w, v.w, q);
+        } else {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + off));
+          x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
         }
       },
       tb, tc, acc0, acc1);
@@ -292,8 +291,8 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, K2_MINB)
       sb[rr] = mont_fin(acc1[4 * h + rr], 2 * ELL, M);
     }
     if (pairs) {
-      const uint4 ea = __ldg(reinterpret_cast<const uint4*>(ev + (size_t)i * N + i0) + h);
-      const uint4 eb = __ldg(reinterpret_cast<const uint4*>(ev + (size_t)(K + i) * N + i0) + h);
+      const uint4 ea = pair_even4(ev, (size_t)i * N + i0 + 4 * h, pairs);
+      const uint4 eb = pair_even4(ev, (size_t)(K + i) * N + i0 + 4 * h, pairs);
       sa[0] = mod_add(sa[0], ea.x, q); sa[1] = mod_add(sa[1], ea.y, q);
       sa[2] = mod_add(sa[2], ea.z, q); sa[3] = mod_add(sa[3], ea.w, q);
       sb[0] = mod_add(sb[0], eb.x, q); sb[1] = mod_add(sb[1], eb.y, q);

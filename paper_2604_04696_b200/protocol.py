@@ -59,7 +59,8 @@ class Context:
         self._slots: dict[int, tuple] = {}   # id(keys) -> (slot, weakref)
         self._free: list[int] = []
         self._next = 0
-        self._lock = threading.Lock()
+        # re-entrant: the weakref callback below may fire (GC) while this thread holds it
+        self._lock = threading.RLock()
 
     def __del__(self):
         try:
@@ -99,10 +100,14 @@ class Context:
             def _gone(_ref, slot=slot, key=id(keys), ctx=weakref.ref(self)):
                 c = ctx()
                 if c is not None and c.h:
+                    # drop in C before the slot becomes reusable: a late drop would
+                    # otherwise empty a slot another key set was just uploaded to
                     with c._lock:
-                        c._slots.pop(key, None)
+                        ent = c._slots.get(key)
+                        if ent is not None and ent[0] == slot:
+                            c._slots.pop(key, None)
+                        c.lib.gpir_keys_drop(c.h, slot)
                         c._free.append(slot)
-                    c.lib.gpir_keys_drop(c.h, slot)
 
             try:
                 ref = weakref.ref(keys, _gone)

@@ -359,3 +359,17 @@ def test_caller_graph_capture(G, golden):
         g.replay()
         torch.cuda.synchronize()
         assert np.array_equal(d_o.cpu().numpy().view(np.uint32).reshape(out0.shape), out0)
+
+
+def test_digits_boundary_vectors(G):
+    """The production-ring (z = 2^22) closed-form digit kernel against the reference's own
+    DigitExtractor on crafted boundary coefficients (tests/golden/digits_boundary.npz,
+    tools/make_digit_golden.py): raw digit == z/2 stays positive, z/2 + 1 carries, carry
+    chains through all ell digits, +-(Q-1)/2."""
+    import os
+
+    from paper_2604_04696_b200 import ops
+    v = np.load(os.path.join(os.path.dirname(__file__), "golden", "digits_boundary.npz"))
+    p = to_api(O.default_params())
+    got = ops.digits(v["coeff"].astype(np.uint64), p.basis, p.gadget)
+    assert np.array_equal(got, v["digits"].astype(np.int64))

@@ -1,5 +1,7 @@
 """Pin the CPU oracle against the golden vectors produced by the live reference
 (tools/make_golden.py).  CPU only."""
+import os
+
 import numpy as np
 import pytest
 
@@ -118,3 +120,13 @@ def test_pipeline_golden(golden, name):
     for (cid, i, j), ct in zip(case["queries"], out):
         m = O.decrypt(clients[cid], ct)
         assert O.decode_plain(m, case["record_bytes"], p) == records[i * case["d1"] + j]
+
+
+def test_digits_boundary_vectors():
+    """Digit-extraction boundary vectors made by the live reference's DigitExtractor and
+    centered_digits_int (tools/make_digit_golden.py): raw digits at z/2 and z/2 + 1 at every
+    position, carry chains through all ell digits, 0, +-1, +-(Q-1)/2."""
+    v = np.load(os.path.join(os.path.dirname(__file__), "golden", "digits_boundary.npz"))
+    p = O.default_params()
+    got = O.gadget_digits(v["coeff"].astype(np.uint64), p.ring, p.z_bits, p.ell)
+    assert np.array_equal(got, v["digits"].astype(np.int64))
