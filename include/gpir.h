@@ -66,6 +66,7 @@ typedef struct gpir_stats {
   float ms_d2h;      /* device->host of responses (host API only) */
   uint32_t launches; /* kernels launched for the batch  */
   float ms_rowsel_kernel; /* RowSel GEMM kernel alone      */
+  float ms_rowsel_transpose; /* RowSel output transpose (P-major -> ciphertexts), 0 if none */
 } gpir_stats;
 
 /* Per-stage device time of the last batch (gpir_set_stage_timing on): one

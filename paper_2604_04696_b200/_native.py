@@ -25,6 +25,7 @@ class GpirStats(C.Structure):
         ("ms_expand", C.c_float), ("ms_rgsw", C.c_float), ("ms_rowsel", C.c_float),
         ("ms_coltor", C.c_float), ("ms_total", C.c_float), ("ms_h2d", C.c_float),
         ("ms_d2h", C.c_float), ("launches", C.c_uint32), ("ms_rowsel_kernel", C.c_float),
+        ("ms_rowsel_transpose", C.c_float),
     ]
 
 

@@ -124,7 +124,7 @@ struct gpir_ctx {
   std::vector<char> slot_rgsw;
   DevBuf evk_pool, rgsw_pool;
   // workspace
-  DevBuf ws_state0, ws_state1, ws_arows, ws_sel, ws_ct0, ws_ct1, ws_kslot, ws_crows;
+  DevBuf ws_state0, ws_state1, ws_arows, ws_sel, ws_ct0, ws_ct1, ws_kslot, ws_crows, ws_y;
   DevBuf ws_coeff, ws_dig, ws_dn, ws_io0, ws_io1, ws_a8;
   int rowsel_engine = 0;  // 0 auto, 1 CUDA cores, 2 tensor cores
   int num_sms = 148;
@@ -132,7 +132,7 @@ struct gpir_ctx {
   u32* sh_leaves = nullptr;
   uint32_t sh_B = 0, sh_d0 = 0, sh_d1 = 0, sh_total = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[12];
+  cudaEvent_t ev[13];
   cudaEvent_t ev_legacy = nullptr;  // orders the private stream after the legacy default stream (pick_stream)
   // CUDA graphs of the device pipeline (answer_dev), keyed by everything the
   // captured launches bake in; the first call of a key runs eagerly (lazy
@@ -718,7 +718,7 @@ struct Engine {
   // output (kernels.cuh PAIRS_IL); *il_out reports whether it was produced.
   static int rowsel(gpir_ctx* c, const u32* leaves, size_t a_b_words, int B, gpir_db* db, u32* sel,
                     cudaStream_t s, uint32_t* launches, cudaEvent_t ev_mid = nullptr, const RsPlan* plan = nullptr,
-                    bool a8_ready = false, bool want_il = false, bool* il_out = nullptr) {
+                    bool a8_ready = false, bool want_il = false, bool* il_out = nullptr, cudaEvent_t ev_y = nullptr) {
     const int KN = K * N;
     int rc;
     if (il_out) *il_out = false;
@@ -735,29 +735,57 @@ struct Engine {
       if (ev_mid) CK(cudaEventRecord(ev_mid, s));
     }
     if (r.kind == 2) {
+      // tensor-core GEMM into the P-major Y[p][m][n], then one transpose pass into the ciphertext layout
+      const size_t ywords = (size_t)KN * r.M * db->d1;
+      if ((rc = c->ws_y.ensure(ywords * 4))) return rc;
       TkArgs ta;
       ta.A8 = c->ws_a8.as<uint8_t>();
       ta.D8 = db->d8.as<uint8_t>();
-      ta.out = sel;
+      ta.out = c->ws_y.as<u32>();
       ta.M = r.M;
       ta.mtiles = r.mtiles;
       ta.d1 = (int)db->d1;
       ta.ntiles = r.ntiles;
+      ta.nt0 = 0;
+      ta.ntiles_db = r.ntiles;
       ta.KN = KN;
       ta.logn = LOGN;
       ta.KC = r.KC;
       ta.units = KN * r.mtiles;
-      ta.out_il = (want_il && db->d1 >= 2) ? 1 : 0;
       const size_t slot = (size_t)128 * r.KC;
       const size_t fixed = (2 * TK_MAX_SLOTS + 16) * 8 + 16;
       ta.slots = std::min<int>(TK_MAX_SLOTS, (int)((226u * 1024u - fixed) / slot));
       const size_t smem = (size_t)ta.slots * slot + fixed;
       if ((rc = set_smem_attr(c, (const void*)k_rowsel_tk, smem))) return rc;
       const int grid = std::min(ta.units, c->num_sms);
-      k_rowsel_tk<<<grid, TC_THREADS, smem, s>>>(ta, c->tb);
+      static const bool tprof_on = getenv("GPIR_TC_PROF") != nullptr;
+      DevBuf tprof;
+      ta.prof = nullptr;
+      if (tprof_on) {
+        if ((rc = tprof.ensure((size_t)grid * 8 * 8))) return rc;
+        CK(cudaMemsetAsync(tprof.p, 0, tprof.bytes, s));
+        ta.prof = tprof.as<unsigned long long>();
+      }
+      k_rowsel_tk<<<grid, TK_THREADS, smem, s>>>(ta, c->tb);
       CKL();
-      ++*launches;
-      if (il_out) *il_out = ta.out_il != 0;
+      if (tprof_on) {
+        std::vector<unsigned long long> h((size_t)grid * 8);
+        CK(cudaMemcpyAsync(h.data(), tprof.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double sum[8] = {0};
+        for (int g = 0; g < grid; ++g)
+          for (int k = 0; k < 8; ++k) sum[k] += (double)h[(size_t)g * 8 + k] / grid;
+        fprintf(stderr, "[tk prof] avg cycles/CTA: mma_wait_drain+A %.0f mma_wait_data %.0f mma_issue_B %.0f epi_wait %.0f epi_work %.0f\n",
+                sum[0], sum[1], sum[2], sum[3], sum[4]);
+        tprof.release();
+      }
+      const int il = (want_il && db->d1 >= 2 && (db->d1 & 1) == 0) ? 1 : 0;
+      if (ev_y) CK(cudaEventRecord(ev_y, s));
+      dim3 tg(KN / YT_P, r.M, ((int)db->d1 + YT_N - 1) / YT_N);
+      k_y_to_cts<<<tg, 256, 0, s>>>(c->ws_y.as<u32>(), r.M, (int)db->d1, KN, sel, (int)db->d1, 0, il);
+      CKL();
+      *launches += 2;
+      if (il_out) *il_out = il != 0;
       return 0;
     }
     if (r.kind == 1) {
@@ -805,6 +833,7 @@ struct Engine {
       if ((rc = set_smem_attr(c, (const void*)kern, smem))) return rc;
       kern<<<grid, TC_THREADS, smem, s>>>(ta, c->tb);
       CKL();
+      if (ev_y) CK(cudaEventRecord(ev_y, s));
       if (prof_on) {
         std::vector<unsigned long long> h((size_t)grid * 8);
         CK(cudaMemcpyAsync(h.data(), profbuf.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -830,6 +859,7 @@ struct Engine {
     k_rowsel_cc<<<grid, 256, RS_SMEM, s>>>(leaves, a_b_words, 2 * B, db->data.as<u32>(), (int)db->d0, (int)db->d1,
                                            sel, KN, LOGN, c->tb);
     CKL();
+    if (ev_y) CK(cudaEventRecord(ev_y, s));
     ++*launches;
     return 0;
   }
@@ -973,7 +1003,7 @@ struct Engine {
     g_sprof.mark(s, "rgsw", 1, 0, xp_default((size_t)B * bits_tree * ELL), (uint32_t)(B * bits_tree * ELL));
     bool il = false;
     if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches,
-                     st ? c->ev[11] : nullptr, &rp, fused, bits > 0, &il)))
+                     st ? c->ev[11] : nullptr, &rp, fused, bits > 0, &il, st ? c->ev[12] : nullptr)))
       return rc;
     if (st) CK(cudaEventRecord(c->ev[4], s));
     g_sprof.mark(s, "rowsel+pack", 2, 0, 0, (uint32_t)B);
@@ -1077,8 +1107,10 @@ struct Engine {
       st->ms_rgsw = a;
       cudaEventElapsedTime(&a, c->ev[3], c->ev[4]);
       st->ms_rowsel = a;
-      cudaEventElapsedTime(&a, c->ev[11], c->ev[4]);
+      cudaEventElapsedTime(&a, c->ev[11], c->ev[12]);
       st->ms_rowsel_kernel = a;
+      cudaEventElapsedTime(&a, c->ev[12], c->ev[4]);
+      st->ms_rowsel_transpose = a;
       cudaEventElapsedTime(&a, c->ev[4], c->ev[5]);
       st->ms_coltor = a;
       cudaEventElapsedTime(&a, c->ev[0], c->ev[6]);
@@ -1588,7 +1620,7 @@ void gpir_ctx_destroy(gpir_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->tw_fwd, &c->tw_inv, &c->mono, &c->evk_pool, &c->rgsw_pool, &c->ws_state0, &c->ws_state1,
-                    &c->ws_arows, &c->ws_sel, &c->ws_ct0, &c->ws_ct1, &c->ws_kslot, &c->ws_coeff, &c->ws_dig,
+                    &c->ws_arows, &c->ws_sel, &c->ws_y, &c->ws_ct0, &c->ws_ct1, &c->ws_kslot, &c->ws_coeff, &c->ws_dig,
                     &c->ws_dn, &c->ws_io0, &c->ws_io1, &c->ws_a8})
     b->release();
   for (auto& ev : c->ev) cudaEventDestroy(ev);

@@ -531,69 +531,92 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tc(TcArgs a, Tables tb
 
 namespace gpir {
 
+
 // ---------------------------------------------------------------------------
 // RowSel with the A operand resident in tensor memory (k_rowsel_tk): the
 // M = 128 row tiles (2B > 64) for d0 <= 256.
 //
 // Work unit = (p, 128-row tile).  The unit's A operand -- 128 rows x KC bytes x
 // 4 byte planes (KC = d0 rounded up to one 32-byte MMA K step) -- is copied
-// into TMEM once (tcgen05.cp, columns [0, KC)) and feeds the MMAs of every
-// 32-column DB tile of that p: A crosses L2 once per unit instead of once per
-// column tile (the r1 kernel re-read it d1/32 times, 6.7x the algorithmic
-// operand bytes at config 3), and per MMA only the 1 KiB B slice is read from
-// shared memory.  The 7 anti-diagonal s32 accumulators (32 columns each, TMEM
-// columns [256, 480)) are single-buffered but issued diagonal by diagonal with
-// one commit per diagonal: the epilogue drains diagonal u of tile t into u64
-// registers while the MMAs of diagonals u+1.. run, and tile t+1 only waits for
-// that drain before its own diagonal u.  The next unit's four A planes are
-// copied in just before the first diagonal that needs them (tcgen05.cp and
-// tcgen05.mma execute in issue order, and plane u was last read by the
-// previous tile's diagonal <= u + 3, dozens of MMAs earlier).
+// into TMEM once (tcgen05.cp, columns [0, 4 KC/4)) and feeds the MMAs of every
+// 32-column DB tile of that p, so A crosses L2 once per unit and per MMA only
+// the 1 KiB B slice is read from shared memory.
+//
+// Accumulators (TMEM columns [256, 512)): eight 32-column s32 slots, the seven
+// anti-diagonals u = s + t of the byte-plane products with the middle one split
+// in two (u = 3 has four products), in two groups of four:
+//   group A = {u1, u5, u3a, u6} (7 products per K step),
+//   group B = {u2, u4, u3b, u0} (9 products per K step).
+// Within a group the MMAs of one K step rotate over its four accumulators so
+// that consecutive MMAs into one accumulator are >= 3 apart: an MMA that
+// accumulates into the previous one's result waits for it (~40 cycles, against
+// 16 per M128 x N32 x K32 MMA back to back; measured: 39 cycles per MMA when a
+// diagonal's MMAs were issued back to back).  Each group has one commit; the
+// epilogue drains group A of tile t while the MMAs of group B run, and the
+// MMAs of tile t+1 only wait for the drain of the same group of tile t, so the
+// single accumulator set (A takes the other 256 columns) stays busy while the
+// epilogue keeps up (one tile = 2048 tensor cycles).
+//
+// Epilogue: 16 warps, four per TMEM lane quadrant, each reducing 8 columns;
+// the diagonals are recombined as lo = C0 + 2^8 C1 + 2^16 C2 + 2^24 C3,
+// hi = C4 + 2^8 C5 + 2^16 C6 (64-bit multiply-adds), x = lo + 2^32 hi mod 2^64 --
+// exact, since the true dot product is < d0 q^2 < 2^64 -- and reduced mod q.
+//
+// Output: the P-major tensor Y[p][m][n] (the window's columns innermost; each
+// thread stores 32 contiguous bytes), transposed afterwards into the ciphertext
+// layout by k_y_to_cts.  The unit owns a single p, so a p-innermost layout
+// could only be written 4-8 bytes at a time.
 //
 // One shared-memory ring of 128 * KC-byte slots carries both the A planes
 // (128 rows x KC) and the DB tiles (4 planes x 32 columns x KC), each one
 // cp.async.bulk: A8[p][mt][plane][KC/16][128][16], D8[p][nt][plane][KC/16][32][16]
-// (UMMA canonical K-major, no swizzle).
-//
-// Output: out_il = 1 writes the ColTor pair layout (the two cts of a ColTor
-// pair interleaved word by word, kernels.cuh PAIRS_IL): the thread of row
-// m = 2b + comp holds 16 columns = 8 pairs of one p and stores each pair as one
-// 8-byte word pair; out_il = 0 writes the standard (B, d1, 2, K*N) layout.
+// (UMMA canonical K-major, no swizzle).  nt0 / ntiles_db select a window of DB
+// column tiles (the capacity path runs RowSel per column chunk).
 constexpr int TK_NT = 32;
 constexpr int TK_ACC0 = 256;  // first accumulator column
 constexpr int TK_MAX_SLOTS = 8;
+constexpr int TK_PF = 6;  // DB tiles prefetched into L2 ahead of the bulk-copy ring
+constexpr int TK_EPI_WARPS = 16;
+constexpr int TK_THREADS = 64 + 32 * TK_EPI_WARPS;
 
 struct TkArgs {
   const uint8_t* A8;
   const uint8_t* D8;
-  u32* out;
-  int M;       // 2B
-  int mtiles;  // 128-row tiles
-  int d1, ntiles, KN, logn;
-  int KC;      // padded K bytes per plane (multiple of 32, <= 256)
-  int units;   // KN * mtiles
-  int slots;   // ring depth
-  int out_il;
+  u32* out;     // Y[p][M][d1]
+  int M;        // 2B
+  int mtiles;   // 128-row tiles
+  int d1;       // columns of the window
+  int ntiles;   // 32-column tiles of the window
+  int nt0, ntiles_db;  // first tile of the window, tiles per p in D8
+  int KN, logn;
+  int KC;       // padded K bytes per plane (multiple of 32, <= 256)
+  int units;    // KN * mtiles
+  int slots;    // ring depth
+  unsigned long long* prof;  // optional per-CTA cycle counters [grid][8] (GPIR_TC_PROF)
 };
 
-__global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb) {
+__device__ __forceinline__ void tk_mma(uint32_t d, uint32_t a, uint64_t b, uint32_t acc) {
+  umma_i8_ta(d, a, b, umma_idesc_u8(128, TK_NT), acc);
+}
+
+__global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb) {
   extern __shared__ __align__(1024) uint8_t tk_smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t slot_bytes = 128u * (uint32_t)a.KC;
   const int NS = a.slots;
   uint64_t* full = reinterpret_cast<uint64_t*>(tk_smem + (size_t)NS * slot_bytes);
   uint64_t* empty = full + TK_MAX_SLOTS;
-  uint64_t* dfull = empty + TK_MAX_SLOTS;
-  uint64_t* dempty = dfull + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 8);
+  uint64_t* dfull = empty + TK_MAX_SLOTS;  // [group]
+  uint64_t* dempty = dfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int u = 0; u < 7; ++u) {
-      mbar_init(&dfull[u], 1);
-      mbar_init(&dempty[u], TC_EPI_WARPS);
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&dfull[g], 1);
+      mbar_init(&dempty[g], TK_EPI_WARPS);
     }
     fence_mbar_init();
   }
@@ -613,7 +636,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
     uint32_t item = 0;
     for (int un = blockIdx.x; un < a.units; un += gridDim.x) {
       const int p = un / a.mtiles, mt = un % a.mtiles;
+      const int nun = un + gridDim.x;
+      if (nun < a.units && lane == 0)  // the next unit's A planes into L2 while this unit runs
+        bulk_prefetch_l2(a.A8 + (size_t)((nun / a.mtiles) * a.mtiles + nun % a.mtiles) * 4 * slot_bytes,
+                         4 * slot_bytes);
       for (int it = 0; it < 4 + a.ntiles; ++it, ++item) {
+        if (lane == 0 && it >= 4 && it + TK_PF < 4 + a.ntiles)  // DB tiles TK_PF ahead of the ring
+          bulk_prefetch_l2(a.D8 + ((size_t)p * a.ntiles_db + a.nt0 + (it + TK_PF - 4)) * slot_bytes, slot_bytes);
         const uint32_t s = item % NS, ph = (item / NS) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         if (elect_one()) {
@@ -623,104 +652,155 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
             bulk_g2s_hint(dst, a.A8 + ((size_t)(p * a.mtiles + mt) * 4 + it) * slot_bytes, slot_bytes, &full[s],
                           pol_once);
           else
-            bulk_g2s(dst, a.D8 + ((size_t)p * a.ntiles + (it - 4)) * slot_bytes, slot_bytes, &full[s]);
+            bulk_g2s(dst, a.D8 + ((size_t)p * a.ntiles_db + a.nt0 + (it - 4)) * slot_bytes, slot_bytes, &full[s]);
         }
         __syncwarp();
       }
     }
   } else if (warp == 1) {  // MMA issuer: one elected thread runs the whole schedule
-    constexpr uint32_t idesc = umma_idesc_u8(128, TK_NT);
     if (elect_one()) {
       uint32_t item = 0, tile = 0;
       const uint32_t acol = (uint32_t)a.KC >> 2;  // TMEM columns per A plane
+      const uint32_t acc0 = tbase + TK_ACC0;
       for (int un = blockIdx.x; un < a.units; un += gridDim.x) {
         const uint32_t item_a = item;  // the unit's A planes: ring items item_a .. item_a + 3
         item += 4;
         for (int nt = 0; nt < a.ntiles; ++nt, ++item, ++tile) {
           const uint32_t sb = item % NS, phb = (item / NS) & 1;
-          const uint32_t bbase = smem_u32(tk_smem + (size_t)sb * slot_bytes);
+          const uint64_t b0 = umma_desc(smem_u32(tk_smem + (size_t)sb * slot_bytes), 512, 128);
+          const uint32_t bpl = (uint32_t)(32 * a.KC) >> 4;  // descriptor step of one B plane
           const uint32_t tph = (tile & 1) ^ 1;
-#pragma unroll 1
-          for (int u = 0; u < 7; ++u) {
-            if (nt == 0 && u < 4) {  // A plane u of this unit into TMEM columns [u * acol, (u + 1) * acol)
-              const uint32_t ia = item_a + u, sa = ia % NS;
+          long long t0 = clock64();
+          if (nt == 0) {  // the unit's four A planes into TMEM columns [sp * acol, (sp + 1) * acol)
+            for (int sp = 0; sp < 4; ++sp) {
+              const uint32_t ia = item_a + sp, sa = ia % NS;
               mbar_wait(&full[sa], (ia / NS) & 1);
               tc_fence_after();
               const uint32_t abase = smem_u32(tk_smem + (size_t)sa * slot_bytes);
               for (int ks = 0; ks < kst; ++ks)
-                tmem_cp_128x256b(tbase + u * acol + 8 * ks, umma_desc(abase + ks * 4096, 2048, 128));
+                tmem_cp_128x256b(tbase + sp * acol + 8 * ks, umma_desc(abase + ks * 4096, 2048, 128));
               umma_commit(&empty[sa]);  // slot free once the copies have landed
             }
-            if (u == 0) {
-              mbar_wait(&full[sb], phb);
-              tc_fence_after();
-            }
-            mbar_wait(&dempty[u], tph);  // diagonal u of the previous tile drained
-            tc_fence_after();
-            const uint32_t dcol = tbase + TK_ACC0 + 32 * u;
-            const int sp0 = u > 3 ? u - 3 : 0, sp1 = u < 3 ? u : 3;
-            for (int sp = sp0; sp <= sp1; ++sp) {
-              const int tp = u - sp;
-              for (int ks = 0; ks < kst; ++ks)
-                umma_i8_ta(dcol, tbase + sp * acol + 8 * ks,
-                           umma_desc(bbase + tp * 32 * a.KC + ks * 1024, 512, 128), idesc,
-                           (sp == sp0 && ks == 0) ? 0u : 1u);
-            }
-            umma_commit(&dfull[u]);
           }
-          umma_commit(&empty[sb]);  // DB tile free once every diagonal has read it
+          mbar_wait(&full[sb], phb);
+          tc_fence_after();
+          long long t1 = clock64();
+          mbar_wait(&dempty[0], tph);  // group A of the previous tile drained
+          tc_fence_after();
+          long long t2 = clock64();
+          // group A (7 products per K step): slots 0..3 = u1, u5, u3a, u6
+          //   (s, t) = (0,1) (2,3) (0,3) (3,3) (1,0) (3,2) (3,0)
+          for (int ks = 0; ks < kst; ++ks) {
+            const uint32_t ak = tbase + 8 * ks;
+            const uint64_t bk = b0 + (uint64_t)(ks * 64);
+            const uint32_t f = ks ? 1u : 0u;
+            tk_mma(acc0 + 0, ak + 0 * acol, bk + 1 * bpl, f);
+            tk_mma(acc0 + 32, ak + 2 * acol, bk + 3 * bpl, f);
+            tk_mma(acc0 + 64, ak + 0 * acol, bk + 3 * bpl, f);
+            tk_mma(acc0 + 96, ak + 3 * acol, bk + 3 * bpl, f);
+            tk_mma(acc0 + 0, ak + 1 * acol, bk + 0 * bpl, 1u);
+            tk_mma(acc0 + 32, ak + 3 * acol, bk + 2 * bpl, 1u);
+            tk_mma(acc0 + 64, ak + 3 * acol, bk + 0 * bpl, 1u);
+          }
+          umma_commit(&dfull[0]);
+          mbar_wait(&dempty[1], tph);  // group B of the previous tile drained
+          tc_fence_after();
+          long long t3 = clock64();
+          // group B (9 products per K step): slots 4..7 = u2, u4, u3b, u0
+          //   (0,2) (1,3) (1,2) (1,1) (2,2) (0,0) (2,0) (3,1) (2,1)
+          for (int ks = 0; ks < kst; ++ks) {
+            const uint32_t ak = tbase + 8 * ks;
+            const uint64_t bk = b0 + (uint64_t)(ks * 64);
+            const uint32_t f = ks ? 1u : 0u;
+            tk_mma(acc0 + 128, ak + 0 * acol, bk + 2 * bpl, f);
+            tk_mma(acc0 + 160, ak + 1 * acol, bk + 3 * bpl, f);
+            tk_mma(acc0 + 192, ak + 1 * acol, bk + 2 * bpl, f);
+            tk_mma(acc0 + 128, ak + 1 * acol, bk + 1 * bpl, 1u);
+            tk_mma(acc0 + 160, ak + 2 * acol, bk + 2 * bpl, 1u);
+            tk_mma(acc0 + 224, ak + 0 * acol, bk + 0 * bpl, f);
+            tk_mma(acc0 + 128, ak + 2 * acol, bk + 0 * bpl, 1u);
+            tk_mma(acc0 + 160, ak + 3 * acol, bk + 1 * bpl, 1u);
+            tk_mma(acc0 + 192, ak + 2 * acol, bk + 1 * bpl, 1u);
+          }
+          umma_commit(&dfull[1]);
+          umma_commit(&empty[sb]);  // DB tile free once both groups have read it
+          if (a.prof) {
+            long long t4 = clock64();
+            a.prof[blockIdx.x * 8 + 1] += t1 - t0;            // waits for data (and the A copies)
+            a.prof[blockIdx.x * 8 + 0] += (t2 - t1) + (t3 - t2 - 0);  // waits for drains + group A issue
+            a.prof[blockIdx.x * 8 + 2] += t4 - t3;            // group B issue
+          }
         }
       }
     }
     __syncwarp();
-  } else {  // epilogue warps 2..9: TMEM lanes 32 * (warp % 4) .., columns 16 * half ..
+  } else {  // epilogue warps 2..17: TMEM lanes 32 * (warp % 4) .., columns 8 * cq ..
     const int quad = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const uint32_t lane_base = tbase + ((uint32_t)(quad * 32) << 16) + TK_ACC0 + 16 * half;
-    const int P2 = a.d1 >> 1;
+    const int cq = (warp - 2) >> 2;
+    const uint32_t lb = tbase + ((uint32_t)(quad * 32) << 16) + TK_ACC0 + 8 * cq;
+    const bool vec = (a.d1 & 3) == 0;
     uint32_t tile = 0;
     for (int un = blockIdx.x; un < a.units; un += gridDim.x) {
       const int p = un / a.mtiles, mt = un % a.mtiles;
       const Modulus M = tb.mod[p >> a.logn];
       const int m = mt * 128 + quad * 32 + lane;
       const bool act = m < a.M;
-      const int b = m >> 1, comp = m & 1;
+      u32* yrow = a.out + ((size_t)p * a.M + (act ? m : 0)) * a.d1;
       for (int nt = 0; nt < a.ntiles; ++nt, ++tile) {
-        u64 acc[16];
+        long long e0 = clock64();
+        mbar_wait(&dfull[0], tile & 1);
+        long long e1 = clock64();
+        tc_fence_after();
+        uint32_t c1[8], c5[8], c3a[8], c6[8];
+        tmem_ld8(lb + 0, c1);
+        tmem_ld8(lb + 32, c5);
+        tmem_ld8(lb + 64, c3a);
+        tmem_ld8(lb + 96, c6);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dempty[0]);
+        u64 lo[8], hi[8];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = 0;
-#pragma unroll
-        for (int u = 0; u < 7; ++u) {
-          mbar_wait(&dfull[u], tile & 1);
-          tc_fence_after();
-          uint32_t v[2][8];
-          tmem_ld8(lane_base + 32 * u, v[0]);
-          tmem_ld8(lane_base + 32 * u + 8, v[1]);
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&dempty[u]);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) acc[j] += (u64)v[j >> 3][j & 7] << (8 * u);
+        for (int j = 0; j < 8; ++j) {
+          lo[j] = (u64)c3a[j] * 16777216u + (u64)c1[j] * 256u;
+          hi[j] = (u64)c6[j] * 65536u + (u64)c5[j] * 256u;
         }
-        if (act) {
-          const int n0 = nt * TK_NT + 16 * half;
-          if (a.out_il) {
+        long long e2 = clock64();
+        mbar_wait(&dfull[1], tile & 1);
+        long long e3 = clock64();
+        tc_fence_after();
+        uint32_t c2[8], c4[8], c3b[8], c0[8];
+        tmem_ld8(lb + 128, c2);
+        tmem_ld8(lb + 160, c4);
+        tmem_ld8(lb + 192, c3b);
+        tmem_ld8(lb + 224, c0);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dempty[1]);
+        u32 r[8];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-              const int pr = (n0 >> 1) + r;
-              if (pr < P2) {
-                u32* dst = a.out + ((((size_t)b * P2 + pr) * 2 + comp) * a.KN + p) * 2;
-                *reinterpret_cast<uint2*>(dst) = make_uint2(reduce_u64(acc[2 * r], M), reduce_u64(acc[2 * r + 1], M));
-              }
-            }
+        for (int j = 0; j < 8; ++j) {
+          const u64 l = lo[j] + (u64)c2[j] * 65536u + (u64)c3b[j] * 16777216u + c0[j];
+          const u64 h = hi[j] + c4[j];
+          r[j] = reduce_u64(l + (h << 32), M);
+        }
+        const int n0 = nt * TK_NT + 8 * cq;
+        if (act) {
+          if (vec && n0 + 8 <= a.d1) {
+            uint4* dst = reinterpret_cast<uint4*>(yrow + n0);
+            dst[0] = make_uint4(r[0], r[1], r[2], r[3]);
+            dst[1] = make_uint4(r[4], r[5], r[6], r[7]);
           } else {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int n = n0 + j;
-              if (n < a.d1) a.out[(((size_t)b * a.d1 + n) * 2 + comp) * a.KN + p] = reduce_u64(acc[j], M);
-            }
+            for (int j = 0; j < 8; ++j)
+              if (n0 + j < a.d1) yrow[n0 + j] = r[j];
           }
+        }
+        if (a.prof && lane == 0 && warp == 2) {
+          a.prof[blockIdx.x * 8 + 3] += (e1 - e0) + (e3 - e2);     // epilogue waits
+          a.prof[blockIdx.x * 8 + 4] += clock64() - e0 - (e1 - e0) - (e3 - e2);  // epilogue work
         }
       }
     }
@@ -729,6 +809,62 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+  }
+}
+
+// Y[p][m][n] (P-major RowSel output of one column window, d1 columns) ->
+// the ciphertext layout (b = m >> 1, comp = m & 1):
+//   il = 0: standard out[((b * d1s + nb + n) * 2 + comp) * KN + p]   (d1s: columns of the full tensor)
+//   il = 1: ColTor pairs interleaved (kernels.cuh PAIRS_IL):
+//           out[(((b * d1s / 2 + (nb + n) / 2) * 2 + comp) * KN + p) * 2 + (n & 1)]
+// One CTA transposes 64 p x 64 columns of one row m through shared memory:
+// 256-byte read runs, 256-byte (il = 0) or 512-byte (il = 1) write runs.
+constexpr int YT_P = 64, YT_N = 64;
+__global__ void __launch_bounds__(256) k_y_to_cts(const u32* __restrict__ Y, int M, int d1, int KN, u32* __restrict__ out,
+                                                  int d1s, int nb, int il) {
+  __shared__ u32 t[YT_N][YT_P + 1];
+  const int p0 = blockIdx.x * YT_P, m = blockIdx.y, n0 = blockIdx.z * YT_N;
+  const int tid = threadIdx.x;
+  const bool vec = (d1 & 3) == 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {  // 64 p rows x 16 chunks of 16 B
+    const int w = tid + 256 * i, row = w >> 4, c4 = w & 15;
+    const int n = n0 + 4 * c4;
+    const u32* src = Y + ((size_t)(p0 + row) * M + m) * d1;
+    if (vec && n + 4 <= d1) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + n));
+      t[4 * c4][row] = v.x, t[4 * c4 + 1][row] = v.y, t[4 * c4 + 2][row] = v.z, t[4 * c4 + 3][row] = v.w;
+    } else {
+      for (int j = 0; j < 4; ++j)
+        if (n + j < d1) t[4 * c4 + j][row] = __ldg(src + n + j);
+    }
+  }
+  __syncthreads();
+  const int b = m >> 1, comp = m & 1;
+  if (il) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {  // 32 pairs x 16 chunks of (4 p x 2 elements)
+      const int w = tid + 256 * i, pr = w >> 4, pq = w & 15;
+      const int n = n0 + 2 * pr;
+      if (n + 1 < d1) {
+        const int gp = (nb + n) >> 1, e = 2 * pr, pp = 4 * pq;
+        uint4* dst =
+            reinterpret_cast<uint4*>(out + ((((size_t)b * (d1s >> 1) + gp) * 2 + comp) * KN + p0 + pp) * 2);
+        dst[0] = make_uint4(t[e][pp], t[e + 1][pp], t[e][pp + 1], t[e + 1][pp + 1]);
+        dst[1] = make_uint4(t[e][pp + 2], t[e + 1][pp + 2], t[e][pp + 3], t[e + 1][pp + 3]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // 64 columns x 16 chunks of 4 p
+      const int w = tid + 256 * i, nl = w >> 4, q4 = w & 15;
+      const int n = n0 + nl;
+      if (n < d1) {
+        const int pp = 4 * q4;
+        *reinterpret_cast<uint4*>(out + (((size_t)b * d1s + nb + n) * 2 + comp) * KN + p0 + pp) =
+            make_uint4(t[nl][pp], t[nl][pp + 1], t[nl][pp + 2], t[nl][pp + 3]);
+      }
+    }
   }
 }
 
