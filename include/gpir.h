@@ -101,6 +101,11 @@ int gpir_set_rowsel_engine(gpir_ctx* ctx, int engine);
  * second call and replay the graph from the third; any device (re)allocation
  * invalidates the recorded graphs. */
 int gpir_set_graphs(gpir_ctx* ctx, int on);
+/* Capacity path knobs (0 = automatic): the bytes the (B, d1) RowSel selection
+ * may occupy before RowSel and the low ColTor stages run per power-of-two
+ * column window (default 16 GiB), and the largest sub-batch served at once
+ * (default: what the free device memory holds).  Results do not change. */
+int gpir_set_capacity(gpir_ctx* ctx, uint64_t sel_budget_bytes, uint32_t max_batch);
 /* Supported (log2 n, k, ell) combinations are compiled in; 1 if supported. */
 int gpir_supported(uint32_t n, uint32_t k, uint32_t ell);
 
@@ -112,6 +117,16 @@ int gpir_supported(uint32_t n, uint32_t k, uint32_t ell);
 gpir_db* gpir_db_encode(gpir_ctx* ctx, const uint8_t* records, uint32_t d0, uint32_t d1, uint32_t record_bytes,
                         uint32_t plain_bits);
 gpir_db* gpir_db_upload(gpir_ctx* ctx, const uint32_t* pmajor, uint32_t d0, uint32_t d1);
+/* encode from records already in device memory (d_records: d0*d1*record_bytes
+ * bytes on the context's device), e.g. generated on the GPU for DBs of many GiB;
+ * same encoding as gpir_db_encode. */
+gpir_db* gpir_db_encode_dev(gpir_ctx* ctx, const uint8_t* d_records, uint32_t d0, uint32_t d1, uint32_t record_bytes,
+                            uint32_t plain_bits);
+/* Capacity mode: keep only the tensor-core byte-plane image of the DB (the
+ * TMEM-resident RowSel layout) and release the u32 copy, so the DB occupies its
+ * encoded size once in HBM (configs 4-5).  Needs d0 <= 256.  A compact DB
+ * cannot be downloaded or saved (GPIR_INVALID_STATE). */
+int gpir_db_compact(gpir_ctx* ctx, gpir_db* db);
 /* GPDB container (wire.save_database / load_database, src/wire.py:365-410):
  * load validates magic, version and the primes against the context (and the
  * plain modulus when expect_plain_bits != 0), streams the payload to the GPU
@@ -123,7 +138,7 @@ int gpir_db_save(gpir_ctx* ctx, const gpir_db* db, const char* path, uint32_t re
 /* Download the encoded DB back as the reference's P-major natural tensor. */
 int gpir_db_download(gpir_ctx* ctx, const gpir_db* db, uint32_t* pmajor_out);
 void gpir_db_destroy(gpir_ctx* ctx, gpir_db* db);
-size_t gpir_db_bytes(const gpir_db* db);
+size_t gpir_db_bytes(const gpir_db* db); /* device bytes held (u32 image + byte planes) */
 
 /* Client key material, stored in key slot `slot`: evks[stages][ell][2][k][n]
  * (stage t uses k_aut = n/2^t + 1, src/he.py:225-241) and sk_rgsw[2 ell][2][k][n]

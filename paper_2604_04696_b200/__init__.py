@@ -15,6 +15,7 @@ from .protocol import (
     answer_batch,
     encode_database,
     encode_database_array,
+    encode_database_device,
     get_context,
     process_batch,
     process_query,
@@ -47,7 +48,8 @@ __all__ = [
     "ExecMode", "ExecutionPlan", "GadgetConfig", "HardwareModel", "HeParams", "InvalidArgument", "InvalidConfig",
     "InvalidState", "LayoutKind", "Modulus", "NativeError", "ParseError", "Phase", "PirError", "Response",
     "RgswCiphertext", "RnsBasis", "RnsPoly", "ServeStats", "answer_batch", "build_plan", "ct_from_raw",
-    "default_basis", "default_params", "encode_database", "encode_database_array", "get_context", "process_batch",
+    "default_basis", "default_params", "encode_database", "encode_database_array", "encode_database_device",
+    "get_context", "process_batch",
     "process_query", "respond", "test_params", "upload_database",
 ]
 

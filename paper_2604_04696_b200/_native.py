@@ -44,8 +44,11 @@ _SIGS = {
     "gpir_ctx_device": (C.c_int, [C.c_void_p]),
     "gpir_set_rowsel_engine": (C.c_int, [C.c_void_p, C.c_int]),
     "gpir_set_graphs": (C.c_int, [C.c_void_p, C.c_int]),
+    "gpir_set_capacity": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32]),
     "gpir_db_encode": (C.c_void_p, [C.c_void_p, _u8p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
     "gpir_db_upload": (C.c_void_p, [C.c_void_p, _u32p, C.c_uint32, C.c_uint32]),
+    "gpir_db_encode_dev": (C.c_void_p, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
+    "gpir_db_compact": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gpir_db_download": (C.c_int, [C.c_void_p, C.c_void_p, _u32p]),
     "gpir_db_destroy": (None, [C.c_void_p, C.c_void_p]),
     "gpir_db_bytes": (C.c_size_t, [C.c_void_p]),

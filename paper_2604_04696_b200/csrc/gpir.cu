@@ -104,6 +104,10 @@ struct gpir_db {
   DevBuf data;  // (d1, d0, k, n) brv
   DevBuf d8;    // tensor-core byte planes D8[p][c][ntile][plane][g][NT][16], packed on first use
   int d8_nt = 0, d8_kc = 0;
+  // capacity mode (gpir_db_compact): only the byte planes in the k_rowsel_tk
+  // layout are kept; the u32 copy is released (the DB then occupies its encoded
+  // size once in HBM) and every batch runs the TMEM-resident RowSel
+  bool compact = false;
 };
 
 struct gpir_ctx {
@@ -115,6 +119,8 @@ struct gpir_ctx {
   TwConst tc{};
   FoldConst fc{};
   int stage_timing = 0;
+  size_t sel_budget = 0;  // capacity path: bytes of the (B, window) RowSel selection (0: env / 16 GiB)
+  int max_batch = 0;      // capacity path: largest sub-batch (0: from the free device memory)
   uint32_t error_bound = 16;
   std::vector<gpir_stage_time> last_stages;
   DevBuf tw_fwd, tw_inv, mono;
@@ -124,7 +130,7 @@ struct gpir_ctx {
   std::vector<char> slot_rgsw;
   DevBuf evk_pool, rgsw_pool;
   // workspace
-  DevBuf ws_state0, ws_state1, ws_arows, ws_sel, ws_ct0, ws_ct1, ws_kslot, ws_crows, ws_y;
+  DevBuf ws_state0, ws_state1, ws_arows, ws_sel, ws_ct0, ws_ct1, ws_kslot, ws_crows, ws_y, ws_part;
   DevBuf ws_coeff, ws_dig, ws_dn, ws_io0, ws_io1, ws_a8;
   int rowsel_engine = 0;  // 0 auto, 1 CUDA cores, 2 tensor cores
   int num_sms = 148;
@@ -635,7 +641,7 @@ struct Engine {
     r.M = 2 * B;
     if (!tc_eligible(c, B, db)) return r;
     static const int tk_env = getenv("GPIR_TK") ? atoi(getenv("GPIR_TK")) : 1;
-    const bool tk = tk_env && r.M > 64 && db->d0 <= 256;
+    const bool tk = db->compact || (tk_env && r.M > 64 && db->d0 <= 256);
     if (tk) {
       r.kind = 2;
       r.RA = 128;
@@ -680,10 +686,60 @@ struct Engine {
     return r;
   }
 
+  // Column window of the capacity path (pipeline): the (B, d1) RowSel selection
+  // and its P-major staging tensor are materialised per window of wd columns
+  // when the whole selection exceeds the budget (GPIR_SEL_BUDGET_GIB, default
+  // 16 GiB; GPIR_D1_WINDOW forces a width).  Windows are power-of-two column
+  // ranges: the tournament pairs columns LSB-first inside each one
+  // (src/planner.py:457-458), so the low log2(wd) ColTor stages run per window.
+  static uint32_t window_d1(gpir_ctx* c, int B, const gpir_db* db, const RsPlan& rp) {
+    const uint32_t d1 = db->d1;
+    if (rp.kind != 2 || d1 <= TK_NT) return d1;
+    static const long wenv = getenv("GPIR_D1_WINDOW") ? atol(getenv("GPIR_D1_WINDOW")) : 0;
+    if (wenv >= TK_NT && (wenv & (wenv - 1)) == 0 && (uint32_t)wenv < d1) return (uint32_t)wenv;
+    static const double genv = getenv("GPIR_SEL_BUDGET_GIB") ? atof(getenv("GPIR_SEL_BUDGET_GIB")) : 16.0;
+    const size_t budget = c->sel_budget ? c->sel_budget : (size_t)(genv * (double)(1ull << 30));
+    const size_t per_col = (size_t)B * CT * 4;
+    uint32_t w = d1;
+    while (w > (uint32_t)TK_NT && (size_t)w * per_col > budget) w >>= 1;
+    return w;
+  }
+
+  // device workspace of one batch of B (bytes, excluding the DB and the key pool)
+  static size_t ws_estimate(gpir_ctx* c, int B, const gpir_db* db) {
+    const uint32_t total = leaves_of(db->d0, db->d1, ELL), bits = ilog2(db->d1);
+    const RsPlan rp = rs_plan(c, B, db);
+    const uint32_t wd = window_d1(c, B, db, rp), nw = db->d1 / wd;
+    const size_t ctb = CT * 4;
+    size_t per = 2 * (size_t)total * ctb + (size_t)3 * std::max<uint32_t>(bits, 1) * ELL * ctb +
+                 (size_t)(wd + std::max<uint32_t>(wd / 2, nw) + wd / 4 + nw) * ctb;
+    if (rp.kind == 2) per += (size_t)wd * ctb;  // P-major staging
+    return (size_t)B * per + rp.a8_bytes + ((size_t)256 << 20);
+  }
+
+  // largest sub-batch that fits the free device memory (GPIR_MAX_BATCH overrides)
+  static int max_subbatch(gpir_ctx* c, int B, const gpir_db* db) {
+    static const int benv = getenv("GPIR_MAX_BATCH") ? atoi(getenv("GPIR_MAX_BATCH")) : 0;
+    if (c->max_batch > 0) return std::min(B, c->max_batch);
+    if (benv > 0) return std::min(B, benv);
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return B;
+    size_t held = 0;
+    for (const DevBuf* b : {&c->ws_state0, &c->ws_state1, &c->ws_arows, &c->ws_sel, &c->ws_y, &c->ws_ct0, &c->ws_ct1,
+                            &c->ws_crows, &c->ws_a8, &c->ws_part})
+      held += b->bytes;
+    const size_t margin = (size_t)4 << 30;
+    const size_t budget = fr + held > margin ? fr + held - margin : 0;
+    int bs = B;
+    while (bs > 1 && ws_estimate(c, bs, db) > budget) bs = (bs + 1) / 2;
+    return bs;
+  }
+
   // DB byte planes D8[p][c][nt][plane][g][NT][16] in the plan's (NT, KC), packed once per layout
   static int ensure_d8(gpir_ctx* c, gpir_db* db, const RsPlan& r, cudaStream_t s) {
     const int KN = K * N;
     if (db->d8_nt == r.NT && db->d8_kc == r.KC) return 0;
+    if (db->compact) FAIL(GPIR_INVALID_STATE, "compact database holds only the TMEM-resident RowSel layout");
     int rc;
     if ((rc = db->d8.ensure((size_t)KN * r.nchunks * r.ntiles * 4 * r.NT * r.KC))) return rc;
     CK(cudaMemsetAsync(db->d8.p, 0, db->d8.bytes, s));
@@ -716,13 +772,18 @@ struct Engine {
   // was already written in the plan's layout into ws_a8 (fused into the last
   // ExpandQuery stage).  want_il: the caller takes the ColTor pair-interleaved
   // output (kernels.cuh PAIRS_IL); *il_out reports whether it was produced.
+  // win_d1 > 0 (k_rowsel_tk only): the column window [win_c0, win_c0 + win_d1) of
+  // the DB (multiples of 32) into sel as a (B, win_d1) tensor -- the capacity path
+  // runs RowSel and the low ColTor stages per window.
   static int rowsel(gpir_ctx* c, const u32* leaves, size_t a_b_words, int B, gpir_db* db, u32* sel,
                     cudaStream_t s, uint32_t* launches, cudaEvent_t ev_mid = nullptr, const RsPlan* plan = nullptr,
-                    bool a8_ready = false, bool want_il = false, bool* il_out = nullptr, cudaEvent_t ev_y = nullptr) {
+                    bool a8_ready = false, bool want_il = false, bool* il_out = nullptr, cudaEvent_t ev_y = nullptr,
+                    int win_c0 = 0, int win_d1 = 0) {
     const int KN = K * N;
     int rc;
     if (il_out) *il_out = false;
     const RsPlan r = plan ? *plan : rs_plan(c, B, db);
+    if (win_d1 && r.kind != 2) FAIL(GPIR_UNSUPPORTED, "column windows need the TMEM-resident RowSel");
     if (r.kind >= 1) {
       if ((rc = ensure_d8(c, db, r, s))) return rc;
       if ((rc = c->ws_a8.ensure(r.a8_bytes))) return rc;
@@ -736,7 +797,8 @@ struct Engine {
     }
     if (r.kind == 2) {
       // tensor-core GEMM into the P-major Y[p][m][n], then one transpose pass into the ciphertext layout
-      const size_t ywords = (size_t)KN * r.M * db->d1;
+      const int wd1 = win_d1 ? win_d1 : (int)db->d1;
+      const size_t ywords = (size_t)KN * r.M * wd1;
       if ((rc = c->ws_y.ensure(ywords * 4))) return rc;
       TkArgs ta;
       ta.A8 = c->ws_a8.as<uint8_t>();
@@ -744,9 +806,9 @@ struct Engine {
       ta.out = c->ws_y.as<u32>();
       ta.M = r.M;
       ta.mtiles = r.mtiles;
-      ta.d1 = (int)db->d1;
-      ta.ntiles = r.ntiles;
-      ta.nt0 = 0;
+      ta.d1 = wd1;
+      ta.ntiles = (wd1 + TK_NT - 1) / TK_NT;
+      ta.nt0 = win_c0 / TK_NT;
       ta.ntiles_db = r.ntiles;
       ta.KN = KN;
       ta.logn = LOGN;
@@ -779,10 +841,10 @@ struct Engine {
                 sum[0], sum[1], sum[2], sum[3], sum[4]);
         tprof.release();
       }
-      const int il = (want_il && db->d1 >= 2 && (db->d1 & 1) == 0) ? 1 : 0;
+      const int il = (want_il && wd1 >= 2 && (wd1 & 1) == 0) ? 1 : 0;
       if (ev_y) CK(cudaEventRecord(ev_y, s));
-      dim3 tg(KN / YT_P, r.M, ((int)db->d1 + YT_N - 1) / YT_N);
-      k_y_to_cts<<<tg, 256, 0, s>>>(c->ws_y.as<u32>(), r.M, (int)db->d1, KN, sel, (int)db->d1, 0, il);
+      dim3 tg(KN / YT_P, r.M, (wd1 + YT_N - 1) / YT_N);
+      k_y_to_cts<<<tg, 256, 0, s>>>(c->ws_y.as<u32>(), r.M, wd1, KN, sel, wd1, 0, il);
       CKL();
       *launches += 2;
       if (il_out) *il_out = il != 0;
@@ -945,15 +1007,18 @@ struct Engine {
   static int xp_default(size_t cts) { return cts >= kXpStageCts ? 3 : 0; }
   static int default_mode(size_t nodes) { return eq_default(nodes); }
 
-  static int ensure_ws(gpir_ctx* c, int B, uint32_t total, uint32_t d1, uint32_t bits) {
+  // wd: the RowSel column window (d1 unless the capacity path splits the columns)
+  static int ensure_ws(gpir_ctx* c, int B, uint32_t total, uint32_t d1, uint32_t bits, uint32_t wd = 0) {
     int rc;
     const size_t ctb = CT * 4;
+    if (!wd) wd = d1;
+    const uint32_t nw = d1 / wd;
     if ((rc = c->ws_state0.ensure((size_t)B * total * ctb))) return rc;
     if ((rc = c->ws_state1.ensure((size_t)B * total * ctb))) return rc;
     if ((rc = c->ws_arows.ensure((size_t)B * std::max<uint32_t>(bits, 1) * ELL * ctb))) return rc;
-    if ((rc = c->ws_sel.ensure((size_t)B * d1 * ctb))) return rc;
-    if ((rc = c->ws_ct0.ensure((size_t)B * std::max<uint32_t>(d1 / 2, 1) * ctb))) return rc;
-    if ((rc = c->ws_ct1.ensure((size_t)B * std::max<uint32_t>(d1 / 4, 1) * ctb))) return rc;
+    if ((rc = c->ws_sel.ensure((size_t)B * wd * ctb))) return rc;
+    if ((rc = c->ws_ct0.ensure((size_t)B * std::max<uint32_t>(std::max(wd / 2, nw / 2), 1) * ctb))) return rc;
+    if ((rc = c->ws_ct1.ensure((size_t)B * std::max<uint32_t>(std::max(wd / 4, nw / 4), 1) * ctb))) return rc;
     if ((rc = c->ws_kslot.ensure((size_t)B * 4))) return rc;
     if ((rc = c->ws_crows.ensure((size_t)B * std::max<uint32_t>(bits, 1) * 2 * ELL * ctb))) return rc;
     return 0;
@@ -980,7 +1045,11 @@ struct Engine {
     RsPlan rp = rs_plan(c, B, db);
     A8Desc a8f = rp.a8;
     bool fused = false;
-    static const bool fuse_env = !getenv("GPIR_FUSE_A8") || atoi(getenv("GPIR_FUSE_A8")) != 0;
+    // The A operand written by the last ExpandQuery stage (k_op_eq_mac_a8) is opt-in
+    // (GPIR_FUSE_A8=1): its 32-byte pieces land 128-256 KiB apart, so the stage costs
+    // more than the separate coalesced pack it replaces (config 2: +0.77 vs 0.46 ms,
+    // config 3: +2.7 vs 1.84 ms, r2 A/B)
+    static const bool fuse_env = getenv("GPIR_FUSE_A8") && atoi(getenv("GPIR_FUSE_A8")) != 0;
     const bool fuse_ok = rp.kind >= 1 && fuse_env && !keep_rows;
     if (fuse_ok) {
       if ((rc = c->ws_a8.ensure(rp.a8_bytes))) return rc;
@@ -1001,6 +1070,52 @@ struct Engine {
     }
     if (st) CK(cudaEventRecord(c->ev[3], s));
     g_sprof.mark(s, "rgsw", 1, 0, xp_default((size_t)B * bits_tree * ELL), (uint32_t)(B * bits_tree * ELL));
+    const uint32_t wd = window_d1(c, B, db, rp);
+    if (wd < d1) {  // capacity path: RowSel + the low log2(wd) ColTor stages per column window
+      if ((rc = fold_coltor(c, B, bits, c->ws_arows.as<u32>(), (size_t)bits_tree * ELL * CT,
+                            leaves + (size_t)d0 * CT, (size_t)total * CT, s)))
+        return rc;
+      const uint32_t nw = d1 / wd, wbits = ilog2(wd);
+      if ((rc = c->ws_part.ensure((size_t)B * nw * CT * 4))) return rc;
+      u32* bufs[2] = {c->ws_ct0.as<u32>(), c->ws_ct1.as<u32>()};
+      for (uint32_t w = 0; w < nw; ++w) {
+        bool il = false;
+        if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches,
+                         (st && w == 0) ? c->ev[11] : nullptr, &rp, fused || w > 0, true, &il,
+                         (st && w == 0) ? c->ev[12] : nullptr, (int)(w * wd), (int)wd)))
+          return rc;
+        if (st && w == 0) CK(cudaEventRecord(c->ev[4], s));
+        u32* cur = c->ws_sel.as<u32>();
+        for (uint32_t j = 0; j < wbits; ++j) {
+          const int C = (int)(wd >> j);
+          const RowsDesc r = coltor_rows(c, bits, j);
+          const int mode = (ct_modes && j < n_ct) ? ct_modes[j] : xp_default((size_t)B * C / 2);
+          const bool last = j + 1 == wbits;
+          u32* dst = last ? c->ws_part.as<u32>() + (size_t)w * CT : bufs[j & 1];
+          if ((rc = ext_product(c, cur, (size_t)C, B, C / 2, (j == 0 && il) ? PAIRS_IL : 1, dst,
+                                last ? (size_t)nw : (size_t)C / 2, r, mode, s, &launches)))
+            return rc;
+          cur = dst;
+        }
+      }
+      g_sprof.mark(s, "rowsel+coltor low (windows of " + std::to_string(wd) + ")", 2, 0, 0, (uint32_t)B);
+      u32* cur = c->ws_part.as<u32>();
+      for (uint32_t j = wbits; j < bits; ++j) {
+        const int C = (int)(d1 >> j);
+        const RowsDesc r = coltor_rows(c, bits, j);
+        const int mode = (ct_modes && j < n_ct) ? ct_modes[j] : xp_default((size_t)B * C / 2);
+        u32* dst = bufs[j & 1];
+        if ((rc = ext_product(c, cur, (size_t)C, B, C / 2, 1, dst, (size_t)C / 2, r, mode, s, &launches))) return rc;
+        g_sprof.mark(s, "coltor" + std::to_string(j) + " " + "oFSH"[mode & 3], 3, (int)j, mode, (uint32_t)(B * C / 2));
+        cur = dst;
+      }
+      if (st) CK(cudaEventRecord(c->ev[5], s));
+      g_sprof.flush(&c->last_stages);
+      *result = cur;
+      if (leaves_out) *leaves_out = leaves;
+      if (st) st->launches += launches;
+      return 0;
+    }
     bool il = false;
     if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches,
                      st ? c->ev[11] : nullptr, &rp, fused, bits > 0, &il, st ? c->ev[12] : nullptr)))
@@ -1039,17 +1154,27 @@ struct Engine {
     const uint32_t total = leaves_of(d0, d1, ELL), bits = ilog2(d1);
     int rc;
     if ((rc = check_keys(c, slots, B, stages_of(total), bits > 0))) return rc;
-    if ((rc = ensure_ws(c, B, total, d1, bits))) return rc;
+    // batches larger than the free memory allows run as consecutive sub-batches
+    // (each reads the DB once more in RowSel; responses do not depend on batch composition)
+    const int Bs = max_subbatch(c, B, db);
+    if ((rc = ensure_ws(c, Bs, total, d1, bits, window_d1(c, Bs, db, rs_plan(c, Bs, db))))) return rc;
+    if ((rc = c->ws_kslot.ensure((size_t)B * 4))) return rc;
     if (st) CK(cudaEventRecord(c->ev[0], s));
     CK(cudaMemcpyAsync(c->ws_kslot.p, slots, (size_t)B * 4, cudaMemcpyHostToDevice, s));
     auto body = [&]() -> int {
       int r;
-      if ((r = bitrev_rows(c, d_q, c->ws_state0.as<u32>(), (size_t)B * 2 * K, s))) return r;
-      u32* res = nullptr;
-      if (st) st->launches += 2;
-      if ((r = pipeline(c, db, d1, B, eq_modes, n_eq, ct_modes, n_ct, c->ws_kslot.as<int>(), s, st, &res, nullptr)))
-        return r;
-      return bitrev_rows(c, res, d_out, (size_t)B * 2 * K, s);
+      for (int b0 = 0; b0 < B; b0 += Bs) {
+        const int nb = std::min(Bs, B - b0);
+        const size_t off = (size_t)b0 * CT;
+        if ((r = bitrev_rows(c, d_q + off, c->ws_state0.as<u32>(), (size_t)nb * 2 * K, s))) return r;
+        u32* res = nullptr;
+        if (st) st->launches += 2;
+        if ((r = pipeline(c, db, d1, nb, eq_modes, n_eq, ct_modes, n_ct, c->ws_kslot.as<int>() + b0, s, st, &res,
+                          nullptr)))
+          return r;
+        if ((r = bitrev_rows(c, res, d_out + off, (size_t)nb * 2 * K, s))) return r;
+      }
+      return 0;
     };
     // graph replay: not with per-phase stats or stage timing (their events and syncs), and
     // not while the caller is itself capturing the stream (the launches then go into its graph)
@@ -1284,6 +1409,21 @@ struct Engine {
                              u32* h_out);
   static int op_xp(gpir_ctx* c, const u32* h_cts, int B, int M, int pairs, const u32* h_rows, int mode, u32* h_out);
   static int op_rowsel(gpir_ctx* c, const u32* h_rows, int B, gpir_db* db, u32* h_out);
+  // capacity mode: pack the byte planes in the k_rowsel_tk layout, release the u32 image
+  static int db_compact(gpir_ctx* c, gpir_db* db) {
+    if (db->compact) return 0;
+    if (db->d0 > 256 || (K * N) % PK_P) FAIL(GPIR_UNSUPPORTED, "compact databases need d0 <= 256");
+    db->compact = true;  // rs_plan: the TMEM-resident RowSel layout for every batch
+    const RsPlan r = rs_plan(c, 128, db);
+    db->compact = false;
+    int rc;
+    if (r.kind != 2) FAIL(GPIR_UNSUPPORTED, "compact databases need the tensor-core RowSel");
+    if ((rc = ensure_d8(c, db, r, c->stream))) return rc;
+    CK(cudaStreamSynchronize(c->stream));
+    db->data.release();
+    db->compact = true;
+    return 0;
+  }
   // client-side material (client.cuh)
   static int client_keygen(gpir_ctx* c, int slot, uint32_t stages, uint64_t seed, int8_t* h_secret);
   static int client_queries(gpir_ctx* c, const int8_t* h_secret, uint32_t plain_bits, uint32_t d0, uint32_t d1,
@@ -1620,7 +1760,7 @@ void gpir_ctx_destroy(gpir_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->tw_fwd, &c->tw_inv, &c->mono, &c->evk_pool, &c->rgsw_pool, &c->ws_state0, &c->ws_state1,
-                    &c->ws_arows, &c->ws_sel, &c->ws_y, &c->ws_ct0, &c->ws_ct1, &c->ws_kslot, &c->ws_coeff, &c->ws_dig,
+                    &c->ws_arows, &c->ws_sel, &c->ws_y, &c->ws_part, &c->ws_ct0, &c->ws_ct1, &c->ws_kslot, &c->ws_coeff, &c->ws_dig,
                     &c->ws_dn, &c->ws_io0, &c->ws_io1, &c->ws_a8})
     b->release();
   for (auto& ev : c->ev) cudaEventDestroy(ev);
@@ -1640,6 +1780,14 @@ int gpir_set_graphs(gpir_ctx* c, int on) {
   return 0;
 }
 
+int gpir_set_capacity(gpir_ctx* c, uint64_t sel_budget_bytes, uint32_t max_batch) {
+  if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->sel_budget = (size_t)sel_budget_bytes;
+  c->max_batch = (int)max_batch;
+  return 0;
+}
+
 int gpir_set_rowsel_engine(gpir_ctx* c, int engine) {
   if (!c || engine < 0 || engine > 2) FAIL(GPIR_INVALID_ARGUMENT, "engine must be 0 (auto), 1 (CUDA cores) or 2 (tensor cores)");
   std::lock_guard<std::mutex> lk(c->mu);
@@ -1647,8 +1795,8 @@ int gpir_set_rowsel_engine(gpir_ctx* c, int engine) {
   return 0;
 }
 
-gpir_db* gpir_db_encode(gpir_ctx* c, const uint8_t* records, uint32_t d0, uint32_t d1, uint32_t record_bytes,
-                        uint32_t plain_bits) {
+static gpir_db* db_encode_impl(gpir_ctx* c, const uint8_t* records, bool on_device, uint32_t d0, uint32_t d1,
+                               uint32_t record_bytes, uint32_t plain_bits) {
   if (!c || !records || !d0 || !d1 || (d1 & (d1 - 1))) {
     g_err = "invalid database geometry";
     return nullptr;
@@ -1664,14 +1812,16 @@ gpir_db* gpir_db_encode(gpir_ctx* c, const uint8_t* records, uint32_t d0, uint32
   db->d1 = d1;
   const size_t recs = (size_t)d0 * d1;
   DevBuf raw;
-  int rc = raw.ensure(std::max<size_t>(recs * record_bytes, 16));
+  int rc = on_device ? 0 : raw.ensure(std::max<size_t>(recs * record_bytes, 16));
   if (!rc) rc = db->data.ensure(recs * c->k * c->n * 4);
-  if (!rc && cudaMemcpyAsync(raw.p, records, recs * record_bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+  if (!rc && !on_device &&
+      cudaMemcpyAsync(raw.p, records, recs * record_bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
     rc = GPIR_CUDA_ERROR, g_err = "db upload failed";
+  const uint8_t* src = on_device ? records : raw.as<uint8_t>();
   if (!rc) {
     switch (c->logn * 100 + c->k) {
 #define ENC(L, K_, E) \
-  case L * 100 + K_: rc = db_encode_launch<L, K_>(c, raw.as<uint8_t>(), (int)record_bytes, (int)d0, (int)d1, (int)plain_bits, db->data.as<u32>(), c->stream); break;
+  case L * 100 + K_: rc = db_encode_launch<L, K_>(c, src, (int)record_bytes, (int)d0, (int)d1, (int)plain_bits, db->data.as<u32>(), c->stream); break;
       GPIR_COMBOS(ENC)
 #undef ENC
       default:
@@ -1686,6 +1836,16 @@ gpir_db* gpir_db_encode(gpir_ctx* c, const uint8_t* records, uint32_t d0, uint32
     return nullptr;
   }
   return db;
+}
+
+gpir_db* gpir_db_encode(gpir_ctx* c, const uint8_t* records, uint32_t d0, uint32_t d1, uint32_t record_bytes,
+                        uint32_t plain_bits) {
+  return db_encode_impl(c, records, false, d0, d1, record_bytes, plain_bits);
+}
+
+gpir_db* gpir_db_encode_dev(gpir_ctx* c, const uint8_t* d_records, uint32_t d0, uint32_t d1, uint32_t record_bytes,
+                            uint32_t plain_bits) {
+  return db_encode_impl(c, d_records, true, d0, d1, record_bytes, plain_bits);
 }
 
 gpir_db* gpir_db_upload(gpir_ctx* c, const uint32_t* pmajor, uint32_t d0, uint32_t d1) {
@@ -1844,8 +2004,21 @@ int gpir_db_save(gpir_ctx* c, const gpir_db* db, const char* path, uint32_t reco
   return 0;
 }
 
+int gpir_db_compact(gpir_ctx* c, gpir_db* db) {
+  if (!c || !db) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  switch (c->logn * 10000 + c->k * 100 + c->ell) {
+    case 120405: return Engine<12, 4, 5>::db_compact(c, db);
+    case 80205: return Engine<8, 2, 5>::db_compact(c, db);
+    case 60206: return Engine<6, 2, 6>::db_compact(c, db);
+    default: FAIL(GPIR_UNSUPPORTED, "unsupported combination");
+  }
+}
+
 int gpir_db_download(gpir_ctx* c, const gpir_db* db, uint32_t* out) {
   if (!c || !db || !out) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
+  if (db->compact) FAIL(GPIR_INVALID_STATE, "compact database: only the byte-plane image is resident");
   std::lock_guard<std::mutex> lk(c->mu);
   CK(cudaSetDevice(c->device));
   const size_t words = (size_t)db->d0 * db->d1 * c->k * c->n;
@@ -1871,7 +2044,7 @@ void gpir_db_destroy(gpir_ctx* c, gpir_db* db) {
   delete db;
 }
 
-size_t gpir_db_bytes(const gpir_db* db) { return db ? db->data.bytes : 0; }
+size_t gpir_db_bytes(const gpir_db* db) { return db ? db->data.bytes + db->d8.bytes : 0; }
 
 // grow the key pools (slots x max stages), preserving existing keys; caller holds c->mu
 static int ensure_key_pool(gpir_ctx* c, int slot, uint32_t stages) {

@@ -216,6 +216,12 @@ class EncodedDatabase:
         pm = self.data if self.layout is LayoutKind.P_MAJOR else self.data.transpose(1, 2, 0)
         return RnsPoly(b, pm[j, i].reshape(b.k, b.n).copy(), Domain.NTT)
 
+    def compact(self) -> "EncodedDatabase":
+        """Capacity mode (gpir_db_compact): keep only the tensor-core byte-plane
+        image in HBM; `data` can no longer be downloaded."""
+        nat.check(self.ctx.lib.gpir_db_compact(self.ctx.h, self.handle), "db compact")
+        return self
+
     def to_layout(self, kind: LayoutKind) -> "EncodedDatabase":
         if kind is self.layout:
             return self
@@ -257,6 +263,29 @@ def encode_database_array(buf: np.ndarray, config: DbConfig, params, kind: Layou
     if not h:
         raise nat.NativeError(f"gpir_db_encode failed: {nat.last_error()}")
     return EncodedDatabase(config, params, ctx, h, kind)
+
+
+def encode_database_device(records, config: DbConfig, params, kind: LayoutKind = LayoutKind.P_MAJOR,
+                           compact: bool = False) -> EncodedDatabase:
+    """Same as `encode_database` from a torch uint8 tensor (records, record_bytes)
+    already on the GPU (gpir_db_encode_dev): DBs of many GiB are generated and
+    encoded on the device.  compact=True keeps only the RowSel byte-plane image."""
+    import torch
+
+    if records.dtype != torch.uint8 or not records.is_cuda or not records.is_contiguous():
+        raise InvalidArgument("records must be a contiguous uint8 CUDA tensor")
+    if tuple(records.shape) != (config.records, config.record_bytes):
+        raise InvalidArgument(f"record tensor shape {tuple(records.shape)} != {(config.records, config.record_bytes)}")
+    if config.record_bytes * 8 > params.basis.n * params.plain_bits:
+        raise InvalidArgument("record does not fit one plaintext polynomial")
+    ctx = get_context(params, records.device.index)
+    torch.cuda.synchronize(records.device)
+    h = ctx.lib.gpir_db_encode_dev(ctx.h, nat.C.c_void_p(records.data_ptr()), config.d0, config.d1,
+                                   config.record_bytes, params.plain_bits)
+    if not h:
+        raise nat.NativeError(f"gpir_db_encode_dev failed: {nat.last_error()}")
+    db = EncodedDatabase(config, params, ctx, h, kind)
+    return db.compact() if compact else db
 
 
 def upload_database(db, device: int | None = None) -> EncodedDatabase:
