@@ -189,6 +189,13 @@ int gpir_plan(gpir_ctx* ctx, uint32_t d0, uint32_t d1, uint32_t B, uint8_t* eq_m
 int gpir_shard_answer(gpir_ctx* ctx, const gpir_db* db, uint32_t d1_total, const uint32_t* d_queries,
                       const int32_t* key_slots, uint32_t B, uint32_t* d_partials, uint32_t* d_high_rgsw,
                       void* stream, gpir_stats* stats);
+/* Column-sharded worker step (the reference's _Worker._answer_shard,
+ * src/cluster.py:252-265): RowSel of B queries' row cts d_rows (internal
+ * layout, (B, d0) from gpir_sharded_expand) against this shard's columns and
+ * the shard's log2(d1) low ColTor stages with d_rgsw_low (B, log2 d1, 2 ell,
+ * 2, k, n) -> d_out (B, 2, k, n).  Large shards run per column window. */
+int gpir_sharded_rowsel_coltor(gpir_ctx* ctx, const gpir_db* db, const uint32_t* d_rows, uint32_t B,
+                               const uint32_t* d_rgsw_low, uint32_t* d_out, void* stream);
 /* Residual tournament: d_cts[B][C][2][k][n] (C power of two) with
  * d_rgsw[B][log2 C][2 ell][2][k][n], natural order -> d_out[B][2][k][n]. */
 int gpir_coltor_dev(gpir_ctx* ctx, const uint32_t* d_cts, uint32_t B, uint32_t C, const uint32_t* d_rgsw,

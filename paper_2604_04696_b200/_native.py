@@ -66,6 +66,8 @@ _SIGS = {
     "gpir_sharded_expand": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, _i32p, C.c_uint32, C.c_void_p,
                                       C.c_void_p]),
     "gpir_sharded_rowsel": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "gpir_sharded_rowsel_coltor": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p,
+                                             C.c_void_p]),
     "gpir_sharded_coltor": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
     "gpir_sharded_rgsw": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
     "gpir_layout_convert": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),

@@ -18,14 +18,20 @@ North-star mode: rank r of n owns DB rows
 Bit-identical to one GPU: RowSel is a sum over rows, split exactly by rows,
 and everything else runs on the query's owner with the same arithmetic.  The
 reference's own multi-worker strategies shard columns (src/cluster.py:5-15,
-350-440); the row split is the north star's, and it shards every phase by n
-(expansion and ColTor by query, RowSel by row) with two collectives whose
-volume does not grow with the DB.
+350-440).  The row split shards every phase by n (expansion and ColTor by
+query, RowSel by row), but its combine moves the partial selection of every
+query and column: the reduce-scatter is (n-1)/n x B x d1 ciphertexts per rank,
+which grows with the DB (56 GiB per rank at config 4, n = 8; `device_comm_bytes`).
+The column split (`answer_col_sharded`) exchanges B x d0 row ciphertexts
+(all-gather) plus B x n partial ciphertexts, independent of d1: it is the mode
+for DBs that do not fit one GPU (configs 4-5), the row split the one for
+DBs that do (configs 1-3, the north star's).
 
-The orchestration (`answer_row_sharded`) is backend- and transport-agnostic so
-the exchange logic is tested on CPU with gloo and the oracle backend
-(tests/test_cluster.py); `CudaRowShard` is the product backend and
-`TorchComm` the NCCL transport.
+The orchestration is backend- and transport-agnostic so the exchange logic is
+tested on CPU with gloo and the oracle backend (tests/test_cluster.py);
+`CudaRowShard` / `CudaColShard` are the product backends, `TorchComm` the NCCL
+transport and `CountingComm` the byte ledger of a run (reference:
+CommLedger / comm_bytes, src/cluster.py:83-141).
 """
 from __future__ import annotations
 
@@ -33,9 +39,101 @@ import ctypes as C
 
 import numpy as np
 
+from dataclasses import dataclass, field
+from enum import Enum
+
 from . import _native as nat
 from .errors import InvalidArgument
 from .protocol import Context, EncodedDatabase
+
+
+class Strategy(Enum):
+    """Multi-worker strategies: the reference's three (src/cluster.py:40-43)
+    plus the north star's row split."""
+    NAIVE_BATCH = "naive"
+    SHARD_AGGREGATE = "shard_aggregate"
+    SHARD_ALL_GATHER = "shard_all_gather"
+    ROW_SHARD = "row_shard"
+
+
+@dataclass
+class CommLedger:
+    """Byte counters for the two synchronization points (src/cluster.py:83-121):
+    after expansion (row ciphertexts) and after the local tournament / RowSel
+    (partials), plus the RGSW sidecar of the all-gather strategy."""
+
+    after_expand_bytes: int = 0
+    after_coltor_bytes: int = 0
+    rgsw_sidecar_bytes: int = 0
+    per_link: dict = field(default_factory=dict, compare=False)
+
+    def add(self, phase: str, worker: int, nbytes: int) -> None:
+        if phase == "expand":
+            self.after_expand_bytes += nbytes
+        elif phase == "coltor":
+            self.after_coltor_bytes += nbytes
+        else:
+            self.rgsw_sidecar_bytes += nbytes
+        key = (worker, phase)
+        self.per_link[key] = self.per_link.get(key, 0) + nbytes
+
+    def modeled_seconds(self, link_bandwidth: float) -> dict:
+        if link_bandwidth <= 0:
+            raise InvalidArgument("link bandwidth must be positive")
+        return {"after_expand": self.after_expand_bytes / link_bandwidth,
+                "after_coltor": self.after_coltor_bytes / link_bandwidth}
+
+    def to_text(self, strategy: Strategy, n_workers: int, link_bandwidth: float | None = None) -> str:
+        rows = [("after_expand", self.after_expand_bytes), ("after_coltor", self.after_coltor_bytes)]
+        lines = ["strategy\tn_workers\tphase\tbytes\tmodeled_seconds"]
+        for phase, nbytes in rows:
+            modeled = f"{nbytes / link_bandwidth:.9f}" if link_bandwidth else "-"
+            lines.append(f"{strategy.value}\t{n_workers}\t{phase}\t{nbytes}\t{modeled}")
+        return "\n".join(lines) + "\n"
+
+
+def comm_bytes(strategy: Strategy, config, batch: int, n_workers: int, params) -> CommLedger:
+    """The reference's closed-form ledger in wire bytes (src/cluster.py:124-136):
+    after_coltor = B n ct; the all-gather strategy adds after_expand = B d0 ct and
+    the RGSW sidecar."""
+    from . import wire
+
+    led = CommLedger()
+    if n_workers <= 1 or strategy in (Strategy.NAIVE_BATCH,):
+        return led
+    ct = wire.serialized_ct_bytes(params)
+    if strategy is Strategy.ROW_SHARD:
+        return device_comm_bytes(strategy, config, batch, n_workers, params)
+    led.after_coltor_bytes = batch * n_workers * ct
+    if strategy is Strategy.SHARD_ALL_GATHER:
+        led.after_expand_bytes = batch * config.d0 * ct
+        body = 6 + 2 * params.basis.k * params.n * 4
+        led.rgsw_sidecar_bytes = batch * (config.d1.bit_length() - 1) * (wire.HEADER_BYTES + 3 + 2 * params.gadget.ell * body)
+    return led
+
+
+def device_comm_bytes(strategy: Strategy, config, batch: int, n_workers: int, params) -> CommLedger:
+    """Bytes the NCCL collectives of this package move between ranks (sum over
+    receiving ranks; a ciphertext is 2 k n u32 words on the device):
+      ROW_SHARD: all-to-all of row blocks (n-1) B d0/n cts, reduce-scatter of the
+                 partial selections (n-1) B d1 cts (it grows with the DB);
+      SHARD_ALL_GATHER: all-gather of row cts (n-1) B d0, of the low-bit RGSW rows
+                 (n-1) B log2(d1/n) 2 ell, all-to-all of partials (n-1)/n B n cts."""
+    led = CommLedger()
+    n = n_workers
+    if n <= 1 or strategy in (Strategy.NAIVE_BATCH, Strategy.SHARD_AGGREGATE):
+        return led
+    ct = 2 * params.basis.k * params.n * 4
+    B, d0, d1 = batch, config.d0, config.d1
+    if strategy is Strategy.ROW_SHARD:
+        led.after_expand_bytes = (n - 1) * B * (d0 // n) * ct
+        led.after_coltor_bytes = (n - 1) * B * d1 * ct
+    else:
+        low = (d1 // n).bit_length() - 1
+        led.after_expand_bytes = (n - 1) * B * d0 * ct
+        led.rgsw_sidecar_bytes = (n - 1) * B * low * 2 * params.gadget.ell * ct
+        led.after_coltor_bytes = (n - 1) * B * ct
+    return led
 
 
 def answer_row_sharded(backend, comm, queries_own, slots_own, d0: int, d1: int):
@@ -55,9 +153,12 @@ def answer_row_sharded(backend, comm, queries_own, slots_own, d0: int, d1: int):
     b_own = rows.shape[0]
     ct = rows.shape[-1]
     d0l = d0 // n
+    mark = getattr(comm, "mark", lambda phase: None)
     send = backend.swap01(rows.reshape(b_own, n, d0l, ct))  # (n, B_own, d0/n, CT)
+    mark("expand")
     recv = comm.all_to_all(send)                      # recv[s] = rank s's queries, my row range
     partial = backend.rowsel(recv.reshape(n * b_own, d0l, ct))
+    mark("coltor")
     sums = comm.reduce_scatter_sum(partial.reshape(n, b_own * d1 * ct))
     return backend.coltor(sums.reshape(b_own, d1, ct))
 
@@ -88,15 +189,19 @@ def answer_col_sharded(backend, comm, queries_own, slots_own, d0: int, d1: int):
     if d1 % n or (n & (n - 1)):
         raise InvalidArgument(f"d1={d1} does not split into {n} power-of-two column shards")
     low = (d1 // n).bit_length() - 1
+    mark = getattr(comm, "mark", lambda phase: None)
     rows, rgsw = backend.expand(queries_own, slots_own)
     b_own = rows.shape[0]
+    mark("expand")
     rows_all = comm.all_gather(rows)                       # (n, B_own, d0, CT), rank order = query order
     if low:
+        mark("rgsw")
         rg_low = comm.all_gather(rgsw[:, :low].contiguous())  # (n, B_own, low, 2 ELL, CT)
     else:
         rg_low = rgsw[:, :0].unsqueeze(0).expand((n,) + tuple(rgsw[:, :0].shape)).contiguous()
     part = backend.rowsel_coltor(rows_all.reshape((n * b_own,) + tuple(rows.shape[1:])),
                                  rg_low.reshape((n * b_own,) + tuple(rg_low.shape[2:])))
+    mark("coltor")
     recv = comm.all_to_all(part.reshape((n, b_own) + tuple(part.shape[1:])))  # recv[s] = shard s's partials
     parts = recv.transpose(0, 1).contiguous()              # (B_own, n, CT): ct index = column shard
     return backend.coltor(parts, rgsw[:, low:].contiguous())
@@ -134,11 +239,71 @@ class TorchComm:
         out = torch.empty(x.shape[1:], dtype=x.dtype, device=x.device)
         try:
             self.dist.reduce_scatter_tensor(out, x, op=self.dist.ReduceOp.SUM, group=self.group)
-        except (RuntimeError, NotImplementedError, ValueError):  # backends without reduce_scatter (gloo)
-            y = x.clone()
-            self.dist.all_reduce(y, op=self.dist.ReduceOp.SUM, group=self.group)
-            out.copy_(y[self.rank])
+        except (RuntimeError, NotImplementedError, ValueError):
+            # backends without reduce_scatter (gloo): block r of every rank to rank r
+            # (the same (n-1)/n volume), summed there
+            recv = self.all_to_all(x.contiguous())
+            out.copy_(recv.sum(dim=0, dtype=x.dtype))
         return out
+
+
+class CountingComm:
+    """Transport wrapper recording the bytes every rank receives from the others
+    into a CommLedger (the measured side of `device_comm_bytes`).  The phase of
+    each collective follows the orchestration: the first exchange of a batch is
+    the row ciphertexts ("expand"), an all-gather of RGSW rows the sidecar, the
+    last exchange the partials ("coltor")."""
+
+    def __init__(self, comm, ledger: CommLedger | None = None):
+        self.comm = comm
+        self.size = comm.size
+        self.rank = getattr(comm, "rank", 0)
+        self.ledger = ledger if ledger is not None else CommLedger()
+        self.phase = "expand"
+
+    def mark(self, phase: str) -> None:
+        """The orchestration names the synchronization point of the next exchange."""
+        self.phase = phase
+
+    def _count(self, nbytes_foreign: int):
+        self.ledger.add(self.phase, self.rank, int(nbytes_foreign))
+
+    def all_to_all(self, send):
+        out = self.comm.all_to_all(send)
+        self._count(send.element_size() * send.numel() * (self.size - 1) // self.size)
+        return out
+
+    def all_gather(self, x):
+        out = self.comm.all_gather(x)
+        self._count(x.element_size() * x.numel() * (self.size - 1))
+        return out
+
+    def reduce_scatter_sum(self, x):
+        out = self.comm.reduce_scatter_sum(x)
+        self._count(x.element_size() * x.numel() * (self.size - 1) // self.size)
+        return out
+
+
+def _encode_shard(ctx, params, recs, cfg, record_bytes: int, compact: bool):
+    """Encode one rank's record shard: a (records, record_bytes) uint8 numpy array
+    (host) or torch CUDA tensor (gpir_db_encode_dev); compact keeps only the
+    RowSel byte planes."""
+    if hasattr(recs, "is_cuda") and recs.is_cuda:
+        if tuple(recs.shape) != (cfg.records, record_bytes):
+            raise InvalidArgument(f"shard shape {tuple(recs.shape)} != {(cfg.records, record_bytes)}")
+        import torch
+        torch.cuda.synchronize(recs.device)
+        h = ctx.lib.gpir_db_encode_dev(ctx.h, C.c_void_p(recs.data_ptr()), cfg.d0, cfg.d1, record_bytes,
+                                       params.plain_bits)
+    else:
+        recs = np.ascontiguousarray(recs, dtype=np.uint8)
+        if recs.shape != (cfg.records, record_bytes):
+            raise InvalidArgument(f"shard shape {recs.shape} != {(cfg.records, record_bytes)}")
+        h = ctx.lib.gpir_db_encode(ctx.h, nat.ptr(recs, C.c_uint8), cfg.d0, cfg.d1, record_bytes, params.plain_bits)
+    if not h:
+        raise nat.NativeError(f"gpir_db_encode failed: {nat.last_error()}")
+    db = EncodedDatabase(cfg, params, ctx, h)
+    return db.compact() if compact else db
 
 
 class CudaRowShard:
@@ -147,7 +312,8 @@ class CudaRowShard:
     `db_rows` is this rank's (d0/n, d1) slice of the record grid (uint8
     array, row-major records); queries/keys are uploaded per call."""
 
-    def __init__(self, params, db_rows: np.ndarray, d0: int, d1: int, record_bytes: int, n: int, device: int):
+    def __init__(self, params, db_rows, d0: int, d1: int, record_bytes: int, n: int, device: int,
+                 compact: bool = False):
         import torch
 
         from .values import DbConfig
@@ -159,14 +325,7 @@ class CudaRowShard:
         # a private context: the sharded session state (expand -> coltor) is per rank
         self.ctx = Context(params, device)
         cfg = DbConfig(d0 // n, d1, record_bytes)
-        recs = np.ascontiguousarray(db_rows, dtype=np.uint8)
-        if recs.shape != (cfg.records, record_bytes):
-            raise InvalidArgument(f"row shard shape {recs.shape} != {(cfg.records, record_bytes)}")
-        h = self.ctx.lib.gpir_db_encode(self.ctx.h, nat.ptr(recs, C.c_uint8), cfg.d0, cfg.d1, record_bytes,
-                                        params.plain_bits)
-        if not h:
-            raise nat.NativeError(f"gpir_db_encode failed: {nat.last_error()}")
-        self.db = EncodedDatabase(cfg, params, self.ctx, h)
+        self.db = _encode_shard(self.ctx, params, db_rows, cfg, record_bytes, compact)
         b = params.basis
         self.ct = 2 * b.k * b.n
         self.stream = torch.cuda.current_stream(device)
@@ -217,7 +376,8 @@ class CudaColShard:
     rank's GPU.  `db_cols` holds this rank's column shard of the record grid as
     a (d0 * d1/n, record_bytes) uint8 array in row-major (i, j_local) order."""
 
-    def __init__(self, params, db_cols: np.ndarray, d0: int, d1: int, record_bytes: int, n: int, device: int):
+    def __init__(self, params, db_cols, d0: int, d1: int, record_bytes: int, n: int, device: int,
+                 compact: bool = False):
         import torch
 
         from .values import DbConfig
@@ -228,14 +388,7 @@ class CudaColShard:
         self.device = device
         self.ctx = Context(params, device)
         cfg = DbConfig(d0, d1 // n, record_bytes)
-        recs = np.ascontiguousarray(db_cols, dtype=np.uint8)
-        if recs.shape != (cfg.records, record_bytes):
-            raise InvalidArgument(f"column shard shape {recs.shape} != {(cfg.records, record_bytes)}")
-        h = self.ctx.lib.gpir_db_encode(self.ctx.h, nat.ptr(recs, C.c_uint8), cfg.d0, cfg.d1, record_bytes,
-                                        params.plain_bits)
-        if not h:
-            raise nat.NativeError(f"gpir_db_encode failed: {nat.last_error()}")
-        self.db = EncodedDatabase(cfg, params, self.ctx, h)
+        self.db = _encode_shard(self.ctx, params, db_cols, cfg, record_bytes, compact)
         b = params.basis
         self.k, self.nn, self.ell = b.k, b.n, params.gadget.ell
         self.ct = 2 * b.k * b.n
@@ -269,17 +422,14 @@ class CudaColShard:
         return rows, rg
 
     def rowsel_coltor(self, rows_all, rgsw_low):
+        # RowSel against this shard's columns + its low ColTor stages in one call
+        # (per column window when the shard's selection exceeds the budget)
         lib, h = self.ctx.lib, self.ctx.h
-        B, d1l = rows_all.shape[0], self.d1 // self.n
-        sel = self._new(B, d1l, self.ct)
-        nat.check(lib.gpir_sharded_rowsel(h, self.db.handle, C.c_void_p(rows_all.data_ptr()), B,
-                                          C.c_void_p(sel.data_ptr()), self._sp()), "sharded rowsel")
-        nat_sel = self._new(B, d1l, self.ct)  # internal slot order -> natural for the tournament
-        nat.check(lib.gpir_layout_convert(h, C.c_void_p(sel.data_ptr()), C.c_void_p(nat_sel.data_ptr()),
-                                          B * d1l * 2, self._sp()), "layout")
+        B = rows_all.shape[0]
         out = self._new(B, self.ct)
-        nat.check(lib.gpir_coltor_dev(h, C.c_void_p(nat_sel.data_ptr()), B, d1l, C.c_void_p(rgsw_low.data_ptr()),
-                                      C.c_void_p(out.data_ptr()), self._sp()), "local coltor")
+        rg = C.c_void_p(rgsw_low.data_ptr()) if rgsw_low.numel() else None
+        nat.check(lib.gpir_sharded_rowsel_coltor(h, self.db.handle, C.c_void_p(rows_all.data_ptr()), B, rg,
+                                                 C.c_void_p(out.data_ptr()), self._sp()), "sharded rowsel+coltor")
         return out
 
     def coltor(self, parts, rgsw_high):

@@ -121,6 +121,31 @@ struct gpir_ctx {
   int stage_timing = 0;
   size_t sel_budget = 0;  // capacity path: bytes of the (B, window) RowSel selection (0: env / 16 GiB)
   int max_batch = 0;      // capacity path: largest sub-batch (0: from the free device memory)
+  // per-phase device time of a batch with stats: intervals between pooled events,
+  // summed over column windows and sub-batches (phase: 0 EQ, 1 RGSW, 2 pack, 3 GEMM,
+  // 4 transpose, 5 ColTor)
+  std::vector<cudaEvent_t> evp;
+  size_t evp_used = 0;
+  struct Interval {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  std::vector<Interval> plog;
+  cudaEvent_t ev_next() {
+    if (evp_used == evp.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      evp.push_back(e);
+    }
+    return evp[evp_used++];
+  }
+  struct SubBatch {
+    const gpir_db* db;
+    int B;
+    uint64_t gen;
+    int bs;
+  };
+  std::vector<SubBatch> subbatch_cache;
   uint32_t error_bound = 16;
   std::vector<gpir_stage_time> last_stages;
   DevBuf tw_fwd, tw_inv, mono;
@@ -722,6 +747,16 @@ struct Engine {
     static const int benv = getenv("GPIR_MAX_BATCH") ? atoi(getenv("GPIR_MAX_BATCH")) : 0;
     if (c->max_batch > 0) return std::min(B, c->max_batch);
     if (benv > 0) return std::min(B, benv);
+    // cached per (db, B) while no device buffer changes (cudaMemGetInfo costs milliseconds per call)
+    const uint64_t gen = g_alloc_gen.load();
+    for (const auto& e : c->subbatch_cache)
+      if (e.db == db && e.B == B && e.gen == gen) return e.bs;
+    const int bs = max_subbatch_probe(c, B, db);
+    if (c->subbatch_cache.size() > 32) c->subbatch_cache.clear();
+    c->subbatch_cache.push_back({db, B, g_alloc_gen.load(), bs});
+    return bs;
+  }
+  static int max_subbatch_probe(gpir_ctx* c, int B, const gpir_db* db) {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return B;
     size_t held = 0;
@@ -841,7 +876,10 @@ struct Engine {
                 sum[0], sum[1], sum[2], sum[3], sum[4]);
         tprof.release();
       }
-      const int il = (want_il && wd1 >= 2 && (wd1 & 1) == 0) ? 1 : 0;
+      // the standard ciphertext layout: ColTor's first stage reads it faster than the pair-interleaved
+      // one (config 3: ColTor 42.3 vs 45.2 ms, r2 A/B), at the same transpose cost
+      static const int il_env = getenv("GPIR_PAIRS_IL") ? atoi(getenv("GPIR_PAIRS_IL")) : 0;
+      const int il = (il_env && want_il && wd1 >= 2 && (wd1 & 1) == 0) ? 1 : 0;
       if (ev_y) CK(cudaEventRecord(ev_y, s));
       dim3 tg(KN / YT_P, r.M, (wd1 + YT_N - 1) / YT_N);
       k_y_to_cts<<<tg, 256, 0, s>>>(c->ws_y.as<u32>(), r.M, wd1, KN, sel, wd1, 0, il);
@@ -1024,6 +1062,17 @@ struct Engine {
     return 0;
   }
 
+  // stats: an event recorded now (nullptr when stats are off)
+  static cudaEvent_t mark(gpir_ctx* c, cudaStream_t s, bool on) {
+    if (!on) return nullptr;
+    cudaEvent_t e = c->ev_next();
+    cudaEventRecord(e, s);
+    return e;
+  }
+  static void span(gpir_ctx* c, int phase, cudaEvent_t a, cudaEvent_t b) {
+    if (a && b) c->plog.push_back({phase, a, b});
+  }
+
   // Full pipeline on device, brv queries already in ws_state0 as (B, 1).
   // Runs expansion over (d0, d1_tree), RGSW assembly for all log2(d1_tree)
   // bits, RowSel on db, and the low log2(db->d1) ColTor stages; returns the
@@ -1037,7 +1086,8 @@ struct Engine {
     const uint32_t bits_tree = ilog2(d1_tree), bits = ilog2(d1);
     uint32_t launches = 0;
     int rc;
-    if (st) CK(cudaEventRecord(c->ev[1], s));
+    const bool on = st != nullptr;
+    cudaEvent_t t_start = mark(c, s, on);
     g_sprof.begin(c->stage_timing != 0);
     g_sprof.mark(s, "start");
     u32* leaves = nullptr;
@@ -1058,7 +1108,8 @@ struct Engine {
     if ((rc = expand_all(c, B, total, eq_modes, n_eq, kslot, &leaves, s, &launches, fuse_ok ? &a8f : nullptr,
                          (int)d0, &fused)))
       return rc;
-    if (st) CK(cudaEventRecord(c->ev[2], s));
+    cudaEvent_t t_eq = mark(c, s, on);
+    span(c, 0, t_start, t_eq);
     // RGSW assembly (src/protocol.py:383-409): a-rows = col_cts ⊡ RGSW(s)
     if (bits_tree > 0) {
       const int M = (int)(bits_tree * ELL);
@@ -1068,7 +1119,8 @@ struct Engine {
                             skrgsw_rows(c, kslot), mode, s, &launches)))
         return rc;
     }
-    if (st) CK(cudaEventRecord(c->ev[3], s));
+    cudaEvent_t t_rgsw = mark(c, s, on);
+    span(c, 1, t_eq, t_rgsw);
     g_sprof.mark(s, "rgsw", 1, 0, xp_default((size_t)B * bits_tree * ELL), (uint32_t)(B * bits_tree * ELL));
     const uint32_t wd = window_d1(c, B, db, rp);
     if (wd < d1) {  // capacity path: RowSel + the low log2(wd) ColTor stages per column window
@@ -1078,13 +1130,17 @@ struct Engine {
       const uint32_t nw = d1 / wd, wbits = ilog2(wd);
       if ((rc = c->ws_part.ensure((size_t)B * nw * CT * 4))) return rc;
       u32* bufs[2] = {c->ws_ct0.as<u32>(), c->ws_ct1.as<u32>()};
+      cudaEvent_t t_w = t_rgsw;
       for (uint32_t w = 0; w < nw; ++w) {
         bool il = false;
-        if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches,
-                         (st && w == 0) ? c->ev[11] : nullptr, &rp, fused || w > 0, true, &il,
-                         (st && w == 0) ? c->ev[12] : nullptr, (int)(w * wd), (int)wd)))
+        cudaEvent_t e_mid = on ? c->ev_next() : nullptr, e_y = on ? c->ev_next() : nullptr;
+        if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches, e_mid, &rp,
+                         fused || w > 0, true, &il, e_y, (int)(w * wd), (int)wd)))
           return rc;
-        if (st && w == 0) CK(cudaEventRecord(c->ev[4], s));
+        cudaEvent_t t_tr = mark(c, s, on);
+        span(c, 2, t_w, e_mid);
+        span(c, 3, e_mid, e_y);
+        span(c, 4, e_y, t_tr);
         u32* cur = c->ws_sel.as<u32>();
         for (uint32_t j = 0; j < wbits; ++j) {
           const int C = (int)(wd >> j);
@@ -1097,6 +1153,8 @@ struct Engine {
             return rc;
           cur = dst;
         }
+        t_w = mark(c, s, on);
+        span(c, 5, t_tr, t_w);
       }
       g_sprof.mark(s, "rowsel+coltor low (windows of " + std::to_string(wd) + ")", 2, 0, 0, (uint32_t)B);
       u32* cur = c->ws_part.as<u32>();
@@ -1109,7 +1167,7 @@ struct Engine {
         g_sprof.mark(s, "coltor" + std::to_string(j) + " " + "oFSH"[mode & 3], 3, (int)j, mode, (uint32_t)(B * C / 2));
         cur = dst;
       }
-      if (st) CK(cudaEventRecord(c->ev[5], s));
+      span(c, 5, t_w, mark(c, s, on));
       g_sprof.flush(&c->last_stages);
       *result = cur;
       if (leaves_out) *leaves_out = leaves;
@@ -1117,10 +1175,14 @@ struct Engine {
       return 0;
     }
     bool il = false;
-    if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches,
-                     st ? c->ev[11] : nullptr, &rp, fused, bits > 0, &il, st ? c->ev[12] : nullptr)))
+    cudaEvent_t e_mid = on ? c->ev_next() : nullptr, e_y = on ? c->ev_next() : nullptr;
+    if ((rc = rowsel(c, leaves, (size_t)total * CT, B, db, c->ws_sel.as<u32>(), s, &launches, e_mid, &rp, fused,
+                     bits > 0, &il, e_y)))
       return rc;
-    if (st) CK(cudaEventRecord(c->ev[4], s));
+    cudaEvent_t t_rs = mark(c, s, on);
+    span(c, 2, t_rgsw, e_mid);
+    span(c, 3, e_mid, e_y);
+    span(c, 4, e_y, t_rs);
     g_sprof.mark(s, "rowsel+pack", 2, 0, 0, (uint32_t)B);
     // ColTor (src/protocol.py:542-573): LSB-first pairs
     if ((rc = fold_coltor(c, B, bits, c->ws_arows.as<u32>(), (size_t)bits_tree * ELL * CT, leaves + (size_t)d0 * CT,
@@ -1139,7 +1201,7 @@ struct Engine {
       g_sprof.mark(s, "coltor" + std::to_string(j) + " " + "oFSH"[mode & 3], 3, (int)j, mode, (uint32_t)(B * C / 2));
       cur = dst;
     }
-    if (st) CK(cudaEventRecord(c->ev[5], s));
+    span(c, 5, t_rs, mark(c, s, on));
     g_sprof.flush(&c->last_stages);
     *result = cur;
     if (leaves_out) *leaves_out = leaves;
@@ -1159,6 +1221,8 @@ struct Engine {
     const int Bs = max_subbatch(c, B, db);
     if ((rc = ensure_ws(c, Bs, total, d1, bits, window_d1(c, Bs, db, rs_plan(c, Bs, db))))) return rc;
     if ((rc = c->ws_kslot.ensure((size_t)B * 4))) return rc;
+    c->evp_used = 0;
+    c->plog.clear();
     if (st) CK(cudaEventRecord(c->ev[0], s));
     CK(cudaMemcpyAsync(c->ws_kslot.p, slots, (size_t)B * 4, cudaMemcpyHostToDevice, s));
     auto body = [&]() -> int {
@@ -1226,22 +1290,28 @@ struct Engine {
       CK(cudaEventRecord(c->ev[6], s));
       CK(cudaEventSynchronize(c->ev[6]));
       float a;
-      cudaEventElapsedTime(&a, c->ev[1], c->ev[2]);
-      st->ms_expand = a;
-      cudaEventElapsedTime(&a, c->ev[2], c->ev[3]);
-      st->ms_rgsw = a;
-      cudaEventElapsedTime(&a, c->ev[3], c->ev[4]);
-      st->ms_rowsel = a;
-      cudaEventElapsedTime(&a, c->ev[11], c->ev[12]);
-      st->ms_rowsel_kernel = a;
-      cudaEventElapsedTime(&a, c->ev[12], c->ev[4]);
-      st->ms_rowsel_transpose = a;
-      cudaEventElapsedTime(&a, c->ev[4], c->ev[5]);
-      st->ms_coltor = a;
+      sum_phases(c, st);
       cudaEventElapsedTime(&a, c->ev[0], c->ev[6]);
       st->ms_total = a;
     }
     return 0;
+  }
+
+  // phase sums of the logged intervals (all windows and sub-batches of the call)
+  static void sum_phases(gpir_ctx* c, gpir_stats* st) {
+    double ph[6] = {0, 0, 0, 0, 0, 0};
+    for (const auto& iv : c->plog) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, iv.a, iv.b) == cudaSuccess) ph[iv.phase] += ms;
+    }
+    st->ms_expand = (float)ph[0];
+    st->ms_rgsw = (float)ph[1];
+    st->ms_rowsel = (float)(ph[2] + ph[3] + ph[4]);
+    st->ms_rowsel_kernel = (float)ph[3];
+    st->ms_rowsel_transpose = (float)ph[4];
+    st->ms_coltor = (float)ph[5];
+    c->plog.clear();
+    c->evp_used = 0;
   }
 
   static int check_keys(gpir_ctx* c, const int32_t* slots, int B, uint32_t stages, bool need_rgsw) {
@@ -1271,8 +1341,14 @@ struct Engine {
     if ((rc = bitrev_rows(c, d_q, c->ws_state0.as<u32>(), (size_t)B * 2 * K, s))) return rc;
     u32* res = nullptr;
     u32* leaves = nullptr;
+    c->evp_used = 0;
+    c->plog.clear();
     if ((rc = pipeline(c, db, d1_total, B, nullptr, 0, nullptr, 0, c->ws_kslot.as<int>(), s, st, &res, &leaves)))
       return rc;
+    if (st) {
+      CK(cudaStreamSynchronize(s));
+      sum_phases(c, st);
+    }
     if ((rc = bitrev_rows(c, res, d_partials, (size_t)B * 2 * K, s))) return rc;
     if (d_high) {
       const uint32_t nh = bits_tree - bits;
@@ -1398,6 +1474,74 @@ struct Engine {
                             xp_default((size_t)B * Cj / 2), s, &launches)))
         return rc;
       cur = dst;
+    }
+    return bitrev_rows(c, cur, d_out, (size_t)B * 2 * K, s);
+  }
+
+  // column-sharded worker step (cluster.answer_col_sharded): RowSel of all B
+  // queries' row cts (brv, (B, d0)) against this shard's columns, then the
+  // shard's log2(d1) ColTor stages with the given low-bit RGSW rows (natural,
+  // (B, bits, 2 ELL)) -> one ct per query (natural).  Uses the capacity path's
+  // column windows when the (B, d1) selection exceeds the budget.
+  static int rowsel_coltor(gpir_ctx* c, gpir_db* db, const u32* d_rows, int B, const u32* d_rgsw, u32* d_out,
+                           cudaStream_t s) {
+    const uint32_t d1 = db->d1, bits = ilog2(d1);
+    int rc;
+    uint32_t launches = 0;
+    if ((rc = c->ws_io0.ensure((size_t)B * std::max<uint32_t>(bits, 1) * 2 * ELL * CT * 4))) return rc;
+    if (bits) {
+      if ((rc = bitrev_rows(c, d_rgsw, c->ws_io0.as<u32>(), (size_t)B * bits * 2 * ELL * 2 * K, s))) return rc;
+      if ((rc = fold_rows(c, c->ws_io0.as<u32>(), c->ws_io0.as<u32>(), B, (int)(2 * bits), (size_t)bits * 2 * ELL * CT,
+                          (size_t)ELL * CT, (size_t)bits * 2 * ELL * CT, (size_t)ELL * CT, s)))
+        return rc;
+    }
+    const RsPlan rp = rs_plan(c, B, db);
+    const uint32_t wd = window_d1(c, B, db, rp), nw = d1 / wd, wbits = ilog2(wd);
+    const size_t ctb = CT * 4;
+    if ((rc = c->ws_sel.ensure(std::max(c->ws_sel.bytes, (size_t)B * wd * ctb)))) return rc;
+    if ((rc = c->ws_ct0.ensure(std::max(c->ws_ct0.bytes, (size_t)B * std::max<uint32_t>(std::max(wd / 2, nw / 2), 1) * ctb))))
+      return rc;
+    if ((rc = c->ws_ct1.ensure(std::max(c->ws_ct1.bytes, (size_t)B * std::max<uint32_t>(std::max(wd / 4, nw / 4), 1) * ctb))))
+      return rc;
+    if ((rc = c->ws_part.ensure(std::max(c->ws_part.bytes, (size_t)B * nw * ctb)))) return rc;
+    auto rows_of = [&](uint32_t j) {
+      RowsDesc r;
+      r.lo = c->ws_io0.as<u32>() + (size_t)j * 2 * ELL * CT;
+      r.lo_b = (size_t)bits * 2 * ELL * CT;
+      r.hi = r.lo + (size_t)ELL * CT;
+      r.hi_b = r.lo_b;
+      r.slot = nullptr;
+      return r;
+    };
+    u32* bufs[2] = {c->ws_ct0.as<u32>(), c->ws_ct1.as<u32>()};
+    u32* cur = nullptr;
+    for (uint32_t w = 0; w < nw; ++w) {
+      bool il = false;
+      if ((rc = rowsel(c, d_rows, (size_t)db->d0 * CT, B, db, c->ws_sel.as<u32>(), s, &launches, nullptr, &rp, w > 0,
+                       bits > 0, &il, nullptr, nw > 1 ? (int)(w * wd) : 0, nw > 1 ? (int)wd : 0)))
+        return rc;
+      cur = c->ws_sel.as<u32>();
+      for (uint32_t j = 0; j < wbits; ++j) {
+        const int C = (int)(wd >> j);
+        const bool last = nw > 1 && j + 1 == wbits;
+        u32* dst = last ? c->ws_part.as<u32>() + (size_t)w * CT : bufs[j & 1];
+        if ((rc = ext_product(c, cur, (size_t)C, B, C / 2, (j == 0 && il) ? PAIRS_IL : 1, dst,
+                              last ? (size_t)nw : (size_t)C / 2, rows_of(j), xp_default((size_t)B * C / 2), s,
+                              &launches)))
+          return rc;
+        cur = dst;
+      }
+    }
+    if (nw > 1) {
+      cur = c->ws_part.as<u32>();
+      for (uint32_t j = wbits; j < bits; ++j) {
+        const int C = (int)(d1 >> j);
+        u32* dst = bufs[j & 1];
+        if ((rc = ext_product(c, cur, (size_t)C, B, C / 2, 1, dst, (size_t)C / 2, rows_of(j),
+                              xp_default((size_t)B * C / 2), s, &launches)))
+          return rc;
+        cur = dst;
+      }
     }
     return bitrev_rows(c, cur, d_out, (size_t)B * 2 * K, s);
   }
@@ -1764,6 +1908,7 @@ void gpir_ctx_destroy(gpir_ctx* c) {
                     &c->ws_dn, &c->ws_io0, &c->ws_io1, &c->ws_a8})
     b->release();
   for (auto& ev : c->ev) cudaEventDestroy(ev);
+  for (auto& ev : c->evp) cudaEventDestroy(ev);
   if (c->ev_legacy) cudaEventDestroy(c->ev_legacy);
   for (auto& g : c->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -2376,6 +2521,26 @@ int gpir_sharded_coltor(gpir_ctx* c, uint32_t* d_sums, uint32_t B, uint32_t* d_o
 #define DISPATCH_CASE_CT(L, K_, E) \
   case L * 10000 + K_ * 100 + E:   \
     rc = Engine<L, K_, E>::coltor_dev(c, d_cts, (int)B, (int)C, d_rgsw, d_out, s); break;
+
+int gpir_sharded_rowsel_coltor(gpir_ctx* c, const gpir_db* db, const uint32_t* d_rows, uint32_t B,
+                               const uint32_t* d_rgsw_low, uint32_t* d_out, void* stream) {
+  if (!c || !db || !d_rows || !d_out || !B) FAIL(GPIR_INVALID_ARGUMENT, "invalid sharded rowsel/coltor input");
+  if (db->d1 > 1 && !d_rgsw_low) FAIL(GPIR_INVALID_ARGUMENT, "missing low-bit RGSW rows");
+  std::lock_guard<std::mutex> lk(c->mu);
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = pick_stream(c, stream);
+  int rc;
+  gpir_db* mdb = const_cast<gpir_db*>(db);
+  switch (c->logn * 10000 + c->k * 100 + c->ell) {
+    case 120405: rc = Engine<12, 4, 5>::rowsel_coltor(c, mdb, d_rows, (int)B, d_rgsw_low, d_out, s); break;
+    case 80205: rc = Engine<8, 2, 5>::rowsel_coltor(c, mdb, d_rows, (int)B, d_rgsw_low, d_out, s); break;
+    case 60206: rc = Engine<6, 2, 6>::rowsel_coltor(c, mdb, d_rows, (int)B, d_rgsw_low, d_out, s); break;
+    default: FAIL(GPIR_UNSUPPORTED, "unsupported combination");
+  }
+  if (rc) return rc;
+  if (!stream) CK(cudaStreamSynchronize(s));
+  return 0;
+}
 
 int gpir_coltor_dev(gpir_ctx* c, const uint32_t* d_cts, uint32_t B, uint32_t C, const uint32_t* d_rgsw,
                     uint32_t* d_out, void* stream) {

@@ -63,7 +63,7 @@ def _material(po, n_queries, seed=3):
 def _rank_main(rank, world, port, out_path):
     import torch.distributed as dist
 
-    from paper_2604_04696_b200.cluster import TorchComm, answer_row_sharded
+    from paper_2604_04696_b200.cluster import CountingComm, TorchComm, answer_row_sharded
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -76,8 +76,11 @@ def _rank_main(rank, world, port, out_path):
     own = slice(rank * B // world, (rank + 1) * B // world)
     be = OracleRowShard(po, db_local, D0, D1, clients[own])
     q_own = torch.from_numpy(qs[own].astype(np.int64))
-    out = answer_row_sharded(be, TorchComm(), q_own, None, D0, D1)
+    cc = CountingComm(TorchComm())
+    out = answer_row_sharded(be, cc, q_own, None, D0, D1)
     np.save(out_path + f".{rank}.npy", out.numpy())
+    np.save(out_path + f".ledger.{rank}.npy", np.array([cc.ledger.after_expand_bytes, cc.ledger.after_coltor_bytes,
+                                                         cc.ledger.rgsw_sidecar_bytes], dtype=np.int64))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -96,6 +99,7 @@ def test_row_sharded_gloo_matches_single_process(tmp_path):
     got = np.concatenate([np.load(path + f".{r}.npy") for r in range(world)]).astype(np.uint64)
     po = O.test_params()
     B = 2 * world
+    _check_ledger(path, world, "row", po, B)
     recs, clients, targets, qs = _material(po, B)
     db = O.encode_database(recs, D0, D1, RB, po)
     want = O.answer_batch(qs, np.stack([c.evks for c in clients]), np.stack([c.sk_rgsw for c in clients]), db,
@@ -104,6 +108,58 @@ def test_row_sharded_gloo_matches_single_process(tmp_path):
     assert np.array_equal(got.reshape(want.shape), want)
     for c, (i, j), ct in zip(clients, targets, want):
         assert O.decode_plain(O.decrypt(c, ct), RB, po) == recs[i * D1 + j]
+
+
+def _check_ledger(path, world, mode, po, B):
+    """The bytes the run's collectives moved (CountingComm, summed over ranks) equal the
+    closed-form device ledger (cluster.device_comm_bytes; reference: comm_bytes,
+    src/cluster.py:124-136).  The oracle backend moves int64 words: 2x the u32 volume."""
+    from paper_2604_04696_b200.cluster import Strategy, device_comm_bytes
+    from paper_2604_04696_b200.values import DbConfig
+    from tests.helpers import to_api
+
+    got = sum(np.load(path + f".ledger.{r}.npy") for r in range(world))
+    st = Strategy.ROW_SHARD if mode == "row" else Strategy.SHARD_ALL_GATHER
+    led = device_comm_bytes(st, DbConfig(D0, D1, RB), B, world, to_api(po))
+    assert list(got) == [2 * led.after_expand_bytes, 2 * led.after_coltor_bytes, 2 * led.rgsw_sidecar_bytes]
+
+
+def test_bench_spawns_ranks_cpu():
+    """`bench.py --gpus 2` re-launches itself under torchrun (2 ranks, 127.0.0.1);
+    the reference arm runs on rank 0 alone and prints one JSON line with n_gpus 2."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--config", "1", "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                       timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference" and d["value"] > 0
+    assert d["config"]["parallelism"].startswith("replica2")  # B = 1 does not split over 2 ranks
+
+
+def test_comm_ledger_closed_forms():
+    """Reference-format ledger (wire bytes, src/cluster.py:124-136) and the device volumes of
+    both sharded modes at config 4 on 8 GPUs."""
+    from paper_2604_04696_b200 import default_params, wire
+    from paper_2604_04696_b200.cluster import Strategy, comm_bytes, device_comm_bytes
+    from paper_2604_04696_b200.values import DbConfig
+
+    p = default_params()
+    cfg = DbConfig(256, 2048, 8192)
+    ct = wire.serialized_ct_bytes(p)
+    led = comm_bytes(Strategy.SHARD_ALL_GATHER, cfg, 256, 8, p)
+    assert led.after_expand_bytes == 256 * 256 * ct and led.after_coltor_bytes == 256 * 8 * ct
+    assert comm_bytes(Strategy.NAIVE_BATCH, cfg, 256, 8, p).after_expand_bytes == 0
+    row = device_comm_bytes(Strategy.ROW_SHARD, cfg, 256, 8, p)
+    assert row.after_coltor_bytes == 7 * 256 * 2048 * 131072  # 56 GiB per rank: grows with the DB
+    col = device_comm_bytes(Strategy.SHARD_ALL_GATHER, cfg, 256, 8, p)
+    assert col.after_expand_bytes == 7 * 256 * 256 * 131072 and col.after_coltor_bytes == 7 * 256 * 131072
 
 
 class _ThreadComm:
@@ -230,7 +286,7 @@ class OracleColShard:
 def _col_rank_main(rank, world, port, out_path):
     import torch.distributed as dist
 
-    from paper_2604_04696_b200.cluster import TorchComm, answer_col_sharded
+    from paper_2604_04696_b200.cluster import CountingComm, TorchComm, answer_col_sharded
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -243,8 +299,11 @@ def _col_rank_main(rank, world, port, out_path):
     own = slice(rank * B // world, (rank + 1) * B // world)
     be = OracleColShard(po, db_local, D0, D1, world, clients[own])
     q_own = torch.from_numpy(qs[own].astype(np.int64))
-    out = answer_col_sharded(be, TorchComm(), q_own, None, D0, D1)
+    cc = CountingComm(TorchComm())
+    out = answer_col_sharded(be, cc, q_own, None, D0, D1)
     np.save(out_path + f".{rank}.npy", out.numpy())
+    np.save(out_path + f".ledger.{rank}.npy", np.array([cc.ledger.after_expand_bytes, cc.ledger.after_coltor_bytes,
+                                                         cc.ledger.rgsw_sidecar_bytes], dtype=np.int64))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -263,6 +322,7 @@ def test_col_sharded_gloo_matches_single_process(tmp_path):
     got = np.concatenate([np.load(path + f".{r}.npy") for r in range(world)]).astype(np.uint64)
     po = O.test_params()
     B = 2 * world
+    _check_ledger(path, world, "col", po, B)
     recs, clients, targets, qs = _material(po, B)
     db = O.encode_database(recs, D0, D1, RB, po)
     want = O.answer_batch(qs, np.stack([c.evks for c in clients]), np.stack([c.sk_rgsw for c in clients]), db,
@@ -312,6 +372,56 @@ def test_col_sharded_gpu_virtual_ranks(world):
     for t in ths:
         t.join()
     got = np.concatenate(outs).astype(np.uint64).reshape(B, 2, po.ring.k, po.n)
+    db = O.encode_database([r.tobytes() for r in recs], d0, d1, rb, po)
+    want = O.answer_batch(qs, np.stack([c.evks for c in clients]), np.stack([c.sk_rgsw for c in clients]), db,
+                          d0, d1, po)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.gpu
+def test_col_sharded_gpu_windows_compact():
+    """Column shards held compact (byte planes only) with the shard's RowSel + low
+    ColTor run per column window (gpir_sharded_rowsel_coltor) on 2 virtual ranks."""
+    from paper_2604_04696_b200 import _native as nat
+    from paper_2604_04696_b200.cluster import CudaColShard, answer_col_sharded
+    from tests.helpers import to_api
+
+    po = O.test_params()
+    p = to_api(po)
+    d0, d1, rb, world = 32, 128, 32, 2
+    B = 4
+    rng = np.random.default_rng(79)
+    recs = rng.integers(0, 256, size=(d0 * d1, rb), dtype=np.uint8)
+    clients = [O.client_keygen(po, d0, d1, rng) for _ in range(B)]
+    targets = [(int(rng.integers(0, d0)), int(rng.integers(0, d1))) for _ in range(B)]
+    qs = np.stack([O.client_query(c, i, j, d0, d1, rng) for c, (i, j) in zip(clients, targets)])
+    comm = _ThreadComm(world)
+    d1l = d1 // world
+    grid = recs.reshape(d0, d1, rb)
+    bes, outs = [], [None] * world
+    R = po.ring
+    for r in range(world):
+        cols = torch.from_numpy(np.ascontiguousarray(grid[:, r * d1l:(r + 1) * d1l]).reshape(d0 * d1l, rb)).cuda()
+        be = CudaColShard(p, cols, d0, d1, rb, world, 0, compact=True)
+        nat.check(be.ctx.lib.gpir_set_capacity(be.ctx.h, B * 32 * 2 * R.k * R.n * 4, 0), "capacity")  # 32-col windows
+        own = range(r * B // world, (r + 1) * B // world)
+        for s_, b in enumerate(own):
+            be.put_keys(s_, clients[b].evks, clients[b].sk_rgsw)
+        bes.append(be)
+
+    def run(r):
+        own = slice(r * B // world, (r + 1) * B // world)
+        q = torch.from_numpy(qs[own].astype(np.uint32).view(np.int32)).cuda()
+        slots = np.arange(B // world, dtype=np.int32)
+        outs[r] = answer_col_sharded(bes[r], comm.view(r), q, slots, d0, d1).cpu().numpy().view(np.uint32)
+        torch.cuda.synchronize()
+
+    ths = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    got = np.concatenate(outs).astype(np.uint64).reshape(B, 2, R.k, R.n)
     db = O.encode_database([r.tobytes() for r in recs], d0, d1, rb, po)
     want = O.answer_batch(qs, np.stack([c.evks for c in clients]), np.stack([c.sk_rgsw for c in clients]), db,
                           d0, d1, po)
