@@ -215,3 +215,38 @@ def phase_model(phase: Phase, config, params, batch: int) -> tuple[int, int]:
             nb += batch * (nodes * 6 * poly + 4 * ell * poly)
         return ops, nb
     raise InvalidArgument(f"unknown phase {phase}")
+
+
+@dataclass(frozen=True)
+class RooflineRow:
+    phase: str
+    ops: int
+    bytes: int
+    ai: float
+    bound: str
+
+
+@dataclass
+class RooflineReport:
+    """Arithmetic intensity of each phase against the platform's ridge point
+    (src/planner.py:273-302), same fields and text format."""
+
+    hw: HardwareModel
+    rows: list
+
+    def to_text(self) -> str:
+        out = [f"ridge_point\t{self.hw.ridge_point:.3f}", "phase\tops\tbytes\tai\tbound"]
+        out += [f"{r.phase}\t{r.ops}\t{r.bytes}\t{r.ai:.4f}\t{r.bound}" for r in self.rows]
+        return "\n".join(out) + "\n"
+
+
+def roofline_report(hw: HardwareModel, config, params, batch: int) -> RooflineReport:
+    """Per-phase ops / bytes from the analytical model (`phase_model`); a phase is
+    compute-bound when its intensity reaches hw.ridge_point.  The measured
+    counterpart on the B200 is bench.py's phase_roofline / roofline."""
+    rows = []
+    for ph in (Phase.EXPAND_QUERY, Phase.ROW_SEL, Phase.COL_TOR):
+        ops, nb = phase_model(ph, config, params, batch)
+        ai = ops / nb
+        rows.append(RooflineRow(ph.value, ops, nb, ai, "compute" if ai >= hw.ridge_point else "memory"))
+    return RooflineReport(hw, rows)

@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as nat
-from . import planner
+from . import layout, planner
 from .errors import InvalidArgument, InvalidState
 from .planner import ExecMode, ExecutionPlan, HardwareModel, Phase
 from .values import (
@@ -418,10 +418,17 @@ def answer_raw(qarr: np.ndarray, client_ids, keys_by_client, db, params, hw: Har
     # per-phase events only when asked for: without them the library replays a
     # captured CUDA graph of the pipeline from the third call of a shape on
     st = nat.GpirStats() if stats is not None else None
+    if stats is not None:  # per-stage CUDA events for ServeStats.stages
+        nat.check(ctx.lib.gpir_set_stage_timing(ctx.h, 1), "stage timing")
     t0 = time.perf_counter()
-    nat.check(ctx.lib.gpir_answer_batch(ctx.h, ddb.handle, nat.ptr(qarr), nat.ptr(slots, nat.C.c_int32), B,
-                                        nat.ptr(em, nat.C.c_uint8), len(em), nat.ptr(cm, nat.C.c_uint8), len(cm),
-                                        nat.ptr(out), nat.C.byref(st) if st is not None else None), "answer_batch")
+    try:
+        nat.check(ctx.lib.gpir_answer_batch(ctx.h, ddb.handle, nat.ptr(qarr), nat.ptr(slots, nat.C.c_int32), B,
+                                            nat.ptr(em, nat.C.c_uint8), len(em), nat.ptr(cm, nat.C.c_uint8),
+                                            len(cm), nat.ptr(out), nat.C.byref(st) if st is not None else None),
+                  "answer_batch")
+    finally:
+        if stats is not None:
+            ctx.lib.gpir_set_stage_timing(ctx.h, 0)
     wall = time.perf_counter() - t0
     if stats is not None:
         stats.add_phase(Phase.EXPAND_QUERY.value, st.ms_expand / 1e3)
@@ -432,7 +439,34 @@ def answer_raw(qarr: np.ndarray, client_ids, keys_by_client, db, params, hw: Har
         stats.h2d_seconds += st.ms_h2d / 1e3
         stats.d2h_seconds += st.ms_d2h / 1e3
         stats.device_seconds += st.ms_total / 1e3
-        stats.stages.append(StageTiming("Batch", 0, B, "gpu", 0, wall, 0))
+        stats.stages.extend(_stage_timings(ctx, config, params, B))
+    return out
+
+
+_PHASE_NAMES = {0: Phase.EXPAND_QUERY.value, 1: "RgswAssembly", 2: Phase.ROW_SEL.value, 3: Phase.COL_TOR.value}
+
+
+def _stage_timings(ctx, config, params, B: int) -> list:
+    """One StageTiming per ExpandQuery stage, RGSW assembly, RowSel and ColTor
+    stage of the last batch (gpir_stage_times; src/protocol.py:301-320, 350-362).
+    mode is the reference's ExecMode value of the executor ("op" / "stage");
+    working_set the reference's transient-bytes model of the stage
+    (planner.working_set) and peak_transient_bytes what the executor
+    materialises in HBM: the working set for operation-level stages, 0 for
+    stage-level ones (their digit NTTs stay on chip)."""
+    buf = (nat.GpirStageTime * 64)()
+    n = ctx.lib.gpir_stage_times(ctx.h, buf, 64)
+    out = []
+    for e in buf[:max(n, 0)]:
+        name = _PHASE_NAMES.get(e.phase, str(e.phase))
+        mode = ExecMode.OPERATION_LEVEL.value if e.mode == 0 else ExecMode.STAGE_LEVEL.value
+        ws = 0
+        if e.phase == 0:
+            ws = planner.working_set(Phase.EXPAND_QUERY, e.stage, B, params, config)
+        elif e.phase == 3:
+            ws = planner.working_set(Phase.COL_TOR, e.stage, B, params, config)
+        out.append(StageTiming(name, int(e.stage), int(e.units), mode, ws, e.ms / 1e3,
+                               ws if e.mode == 0 else 0))
     return out
 
 
@@ -447,6 +481,11 @@ def answer_batch(queries, keys_by_client, db, params, hw: HardwareModel | None =
         return []
     if engine not in _ENGINES:
         raise InvalidArgument(f"unknown row-selection engine {engine!r}")
+    if tile is not None or pipeline is not None:
+        lay = "p_major" if getattr(getattr(db, "layout", None), "value", "pmajor") in ("pmajor", "p_major") \
+            else "transposed"
+        b = params.basis
+        layout.validate_rowsel(engine, lay, 2 * len(queries), db.config.d1, db.config.d0, b.k, b.n, tile, pipeline)
     for q in queries:
         if q.client_id not in keys_by_client:
             raise InvalidState(f"no uploaded keys for client {q.client_id}")
