@@ -436,13 +436,14 @@ struct Engine {
 
   // op-level scratch sizing: nodes per chunk bounded by ~1 GiB
   static size_t op_chunk(size_t per_node_words) {
-    const size_t budget = (size_t)1 << 29;  // words (2 GiB): a whole config-2 stage in one chunk
+    static const double genv = getenv("GPIR_OP_BUDGET_GIB") ? atof(getenv("GPIR_OP_BUDGET_GIB")) : 2.0;
+    const size_t budget = (size_t)(genv * (double)(1ull << 28));  // words (default 2 GiB): a config-2 stage per chunk
     return std::max<size_t>(1, budget / per_node_words);
   }
 
   // one ExpandQuery stage: state (B, C) -> out (B, Cout)
   // a8f (operation-level mode only): write the row leaves (outputs c < d0) as
-  // RowSel byte planes in that layout instead of u32 words (k_op_eq_mac_a8)
+  // RowSel byte planes in that layout instead of u32 words (k_op_eq_mac_a8q)
   static int expand_stage(gpir_ctx* c, const u32* state, int B, int C, u32* out, int Cout, int t, RowsDesc ksk,
                           int mode, cudaStream_t s, uint32_t* launches, const A8Desc* a8f = nullptr, int d0 = 0) {
     const u32 k_aut = (u32)(N >> t) + 1;
@@ -475,6 +476,7 @@ struct Engine {
     static const size_t chunk_env = getenv("GPIR_OP_CHUNK") ? (size_t)atol(getenv("GPIR_OP_CHUNK")) : 0;
     size_t chunk = chunk_env ? chunk_env : op_chunk(per);
     if (chunk >= 16) chunk &= ~(size_t)15;  // node groups of the batched MACs never straddle a chunk
+    if (a8f) chunk = std::max<size_t>(1, chunk / C) * C;  // the fused last stage: whole queries per chunk
     const size_t nodes = (size_t)B * C;
     const size_t cn = std::min(chunk, nodes);
     if ((rc = c->ws_coeff.ensure(cn * K * N * 4))) return rc;
@@ -503,17 +505,25 @@ struct Engine {
       CKL();
       if (g_sprof.fine) g_sprof.mark(s, "  eq_dntt");
       static const int mac_nb = getenv("GPIR_MAC_NB") ? atoi(getenv("GPIR_MAC_NB")) : 108;
-      if (a8f) {  // last stage: row leaves straight into the RowSel A operand
-        const size_t tm = (size_t)(nn / 16) * K * N;
-        k_op_eq_mac_a8<LOGN, K, ELL><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(
-            state, C, (int)n0, nn, c->ws_dn.as<u32>(), ksk, k_aut, mono, out, Cout, c->tb, *a8f, d0);
+      if (a8f) {  // last stage: row leaves straight into the RowSel A operand (+ the other nodes as usual)
+        const int b0 = (int)(n0 / C), nq = nn / C;
+        dim3 g((N / 8) * K, (nq + 31) / 32, d0 / 16);
+        k_op_eq_mac_a8q<LOGN, K, ELL><<<g, 256, 0, s>>>(state, C, b0, nq, c->ws_dn.as<u32>(), ksk, k_aut, mono, out,
+                                                        Cout, c->tb, *a8f);
+        if (d0 < C) {
+          CKL();
+          const size_t tm = ((size_t)(nn + 7) / 8) * K * (N / 4);
+          k_op_eq_mac_nb4<LOGN, K, ELL, 8><<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(
+              state, C, (int)n0, nn, c->ws_dn.as<u32>(), ksk, k_aut, mono, out, Cout, c->tb, d0);
+          ++*launches;
+        }
       } else if (mac_nb == 4 || mac_nb == 104 || mac_nb == 108 || mac_nb == 116) {  // 4 slots per thread, NB nodes
         const int nb = mac_nb == 4 ? 4 : mac_nb - 100;
         const size_t tm = ((size_t)(nn + nb - 1) / nb) * K * (N / 4);
         auto kern = nb == 4 ? k_op_eq_mac_nb4<LOGN, K, ELL, 4>
                     : nb == 8 ? k_op_eq_mac_nb4<LOGN, K, ELL, 8> : k_op_eq_mac_nb4<LOGN, K, ELL, 16>;
         kern<<<(unsigned)((tm + 255) / 256), 256, 0, s>>>(state, C, (int)n0, nn, c->ws_dn.as<u32>(), ksk, k_aut,
-                                                           mono, out, Cout, c->tb);
+                                                           mono, out, Cout, c->tb, 0);
       } else if (mac_nb == 8 || mac_nb == 16 || mac_nb == 32) {  // NB nodes per thread: key rows loaded once per group
         const size_t tm = ((size_t)(nn + mac_nb - 1) / mac_nb) * K * N;
         auto kern = mac_nb == 8 ? k_op_eq_mac_nb<LOGN, K, ELL, 8>
@@ -653,7 +663,7 @@ struct Engine {
   //   kind 1: tensor cores, operands streamed per K chunk (k_rowsel_tc: M = 64 tiles, or d0 > 256);
   //   kind 2: tensor cores, A resident in TMEM (k_rowsel_tk: 2B > 64, d0 <= 256).
   // The A operand's byte-plane layout (a8) is fixed here so the last ExpandQuery
-  // stage can write it directly (k_op_eq_mac_a8).
+  // stage can write it directly (k_op_eq_mac_a8q, opt-in).
   struct RsPlan {
     int kind = 0;
     int M = 0, RA = 0, mtiles = 0, NT = 0, KC = 0, nchunks = 0, ntiles = 0, PST = 0;
@@ -1095,10 +1105,10 @@ struct Engine {
     RsPlan rp = rs_plan(c, B, db);
     A8Desc a8f = rp.a8;
     bool fused = false;
-    // The A operand written by the last ExpandQuery stage (k_op_eq_mac_a8) is opt-in
-    // (GPIR_FUSE_A8=1): its 32-byte pieces land 128-256 KiB apart, so the stage costs
-    // more than the separate coalesced pack it replaces (config 2: +0.77 vs 0.46 ms,
-    // config 3: +2.7 vs 1.84 ms, r2 A/B)
+    // The A operand written by the last ExpandQuery stage (k_op_eq_mac_a8q) is opt-in
+    // (GPIR_FUSE_A8=1): its one-slot-per-thread MAC (coalesced byte-plane writes need
+    // lanes over queries) costs more than the separate coalesced pack it replaces
+    // (config 2: ExpandQuery +1.05 vs pack 0.46 ms, config 3: +4.6 vs 1.84 ms, r2 A/B)
     static const bool fuse_env = getenv("GPIR_FUSE_A8") && atoi(getenv("GPIR_FUSE_A8")) != 0;
     const bool fuse_ok = rp.kind >= 1 && fuse_env && !keep_rows;
     if (fuse_ok) {

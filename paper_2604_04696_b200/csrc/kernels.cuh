@@ -801,7 +801,7 @@ template <int LOGN, int K, int ELL, int NB>
 __global__ void __launch_bounds__(256) k_op_eq_mac_nb4(const u32* __restrict__ state, int C, int node0, int nodes,
                                                        const u32* __restrict__ dn, RowsDesc ksk, u32 k_aut,
                                                        const uint2* __restrict__ mono, u32* __restrict__ out, int Cout,
-                                                       Tables tb) {
+                                                       Tables tb, int skip_c = 0) {
   constexpr int N = 1 << LOGN;
   const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t groups = ((size_t)nodes + NB - 1) / NB;
@@ -823,6 +823,7 @@ __global__ void __launch_bounds__(256) k_op_eq_mac_nb4(const u32* __restrict__ s
     if (nd >= nodes) break;
     const int gn = node0 + nd;
     const int b = gn / C, c = gn % C;
+    if (c < skip_c) continue;  // a row node: written by k_op_eq_mac_a8q
     if (b != cur_b) {
 #pragma unroll
       for (int j = 0; j < ELL; ++j) {
@@ -894,34 +895,34 @@ struct A8Desc {
   }
 };
 
-// (4a-iv) the LAST ExpandQuery stage's MAC + combine with the RowSel operand
-// pack fused in (_expanded_to_in0 + transpose_ct_tensor, src/protocol.py:426-441,
-// src/layout.py:156-178): 16 consecutive nodes of one query per thread, one
-// slot.  The `c + s` outputs of nodes c < d0 are the row ciphertexts; instead
-// of their u32 words the thread writes their byte planes -- 16 nodes = one
-// 16-byte K group per (row, plane) -- straight into the A operand (a8), so
-// RowSel needs no separate packing pass over the row leaves.  Requires
-// node0 % 16 == 0, C % 16 == 0, d0 % 16 == 0 and d0 <= C (rows only among the
-// first outputs); all other outputs are written as usual.
+// (4a-v) the LAST ExpandQuery stage's MAC + combine for the row nodes (c < d0)
+// with the RowSel operand pack fused in (_expanded_to_in0 + transpose_ct_tensor,
+// src/protocol.py:426-441, src/layout.py:156-178), laid out for coalesced
+// byte-plane writes: a warp covers 8 consecutive slots x 4 consecutive queries,
+// a CTA 8 slots x 32 queries, and each thread 16 consecutive nodes (one 16-byte
+// K group) of one slot.  The c + s outputs go to the A operand only -- per
+// (slot, plane) the warp writes rows 2b .. 2b + 7 of one K group, 128
+// contiguous bytes, the CTA 512 -- and the X^{-2^t} (c - s) outputs (c + C <
+// Cout) as u32 words.  Grid: x = (N / 8) x K, y = ceil(nq / 32) over the chunk's
+// queries [b0, b0 + nq), z = d0 / 16 node groups; dn holds the chunk's digit NTTs
+// with node index (b - b0) C + c.  Requires d0 % 16 == 0 and d0 <= C.
 template <int LOGN, int K, int ELL>
-__global__ void __launch_bounds__(256) k_op_eq_mac_a8(const u32* __restrict__ state, int C, int node0, int nodes,
-                                                      const u32* __restrict__ dn, RowsDesc ksk, u32 k_aut,
-                                                      const uint2* __restrict__ mono, u32* __restrict__ out, int Cout,
-                                                      Tables tb, A8Desc a8, int d0) {
+__global__ void __launch_bounds__(256) k_op_eq_mac_a8q(const u32* __restrict__ state, int C, int b0, int nq,
+                                                       const u32* __restrict__ dn, RowsDesc ksk, u32 k_aut,
+                                                       const uint2* __restrict__ mono, u32* __restrict__ out, int Cout,
+                                                       Tables tb, A8Desc a8) {
   constexpr int N = 1 << LOGN;
-  const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const size_t groups = (size_t)nodes / 16;
-  if (g >= groups * K * N) return;
-  const int pos = (int)(g & (N - 1));
-  const int i = (int)((g >> LOGN) % K);
-  const int nd0 = (int)(g / ((size_t)K * N)) * 16;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pos = (int)(blockIdx.x % (N / 8)) * 8 + (lane & 7);
+  const int i = (int)(blockIdx.x / (N / 8));
+  const int bl = (int)blockIdx.y * 32 + warp * 4 + (lane >> 3);
+  if (bl >= nq) return;
+  const int b = b0 + bl, c0 = (int)blockIdx.z * 16;
   const size_t CT = 2 * (size_t)K * N;
   const Modulus M = tb.mod[i];
   const u32 q = M.q;
   const u32 src_pos = aut_src(pos, k_aut, LOGN);
   const uint2 w = __ldg(&mono[(size_t)i * N + pos]);
-  const int gn0 = node0 + nd0;
-  const int b = gn0 / C, c0 = gn0 % C;
   u32 ka[ELL], kb[ELL];
 #pragma unroll
   for (int j = 0; j < ELL; ++j) {
@@ -929,7 +930,6 @@ __global__ void __launch_bounds__(256) k_op_eq_mac_a8(const u32* __restrict__ st
     ka[j] = __ldg(ra);
     kb[j] = __ldg(ra + (size_t)K * N);
   }
-  const bool rows = c0 < d0;
   u32 pa[4][4], pb[4][4];  // [plane][word]: byte u of the 16-byte K group = node c0 + u
 #pragma unroll
   for (int pl = 0; pl < 4; ++pl)
@@ -937,13 +937,13 @@ __global__ void __launch_bounds__(256) k_op_eq_mac_a8(const u32* __restrict__ st
     for (int v = 0; v < 4; ++v) pa[pl][v] = pb[pl][v] = 0;
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
-    const int nd = nd0 + u;
     const int c = c0 + u;
-    const u32* st = state + (size_t)(gn0 + u) * CT;
+    const size_t nd = (size_t)bl * C + c;
+    const u32* st = state + ((size_t)b * C + c) * CT;
     u64 a0 = 0, a1 = 0;
 #pragma unroll
     for (int j = 0; j < ELL; ++j) {  // digit ELL-1 is folded: its term is tau(a) itself
-      const u32 d = j < ELL - 1 ? __ldg(dn + (((size_t)nd * ELL + j) * K + i) * N + pos) : __ldg(st + (size_t)i * N + src_pos);
+      const u32 d = j < ELL - 1 ? __ldg(dn + ((nd * ELL + j) * K + i) * N + pos) : __ldg(st + (size_t)i * N + src_pos);
       a0 += (u64)d * ka[j];
       a1 += (u64)d * kb[j];
     }
@@ -951,16 +951,10 @@ __global__ void __launch_bounds__(256) k_op_eq_mac_a8(const u32* __restrict__ st
     const u32 sa = reduce_u64(a0, M);
     const u32 sb = mod_add(reduce_u64(a1, M), __ldg(st + (size_t)(K + i) * N + src_pos), q);
     const u32 xa = mod_add(ca, sa, q), xb = mod_add(cb, sb, q);
-    if (rows) {
 #pragma unroll
-      for (int pl = 0; pl < 4; ++pl) {
-        pa[pl][u >> 2] |= ((xa >> (8 * pl)) & 0xffu) << (8 * (u & 3));
-        pb[pl][u >> 2] |= ((xb >> (8 * pl)) & 0xffu) << (8 * (u & 3));
-      }
-    } else {
-      u32* o0 = out + ((size_t)b * Cout + c) * CT;
-      o0[(size_t)i * N + pos] = xa;
-      o0[(size_t)(K + i) * N + pos] = xb;
+    for (int pl = 0; pl < 4; ++pl) {
+      pa[pl][u >> 2] |= ((xa >> (8 * pl)) & 0xffu) << (8 * (u & 3));
+      pb[pl][u >> 2] |= ((xb >> (8 * pl)) & 0xffu) << (8 * (u & 3));
     }
     if (c + C < Cout) {
       u32* o1 = out + ((size_t)b * Cout + c + C) * CT;
@@ -968,14 +962,12 @@ __global__ void __launch_bounds__(256) k_op_eq_mac_a8(const u32* __restrict__ st
       o1[(size_t)(K + i) * N + pos] = csub(mul_shoup(mod_sub(cb, sb, q), w.x, w.y, q), q);
     }
   }
-  if (rows) {
-    const int p = i * N + pos, kg = c0 >> 4;
+  const int p = i * N + pos, kg = c0 >> 4;
 #pragma unroll
-    for (int pl = 0; pl < 4; ++pl) {
-      uint4* d = reinterpret_cast<uint4*>(a8.at(p, 2 * b, kg, pl));  // rows 2b, 2b + 1: one 32-byte sector
-      d[0] = make_uint4(pa[pl][0], pa[pl][1], pa[pl][2], pa[pl][3]);
-      d[1] = make_uint4(pb[pl][0], pb[pl][1], pb[pl][2], pb[pl][3]);
-    }
+  for (int pl = 0; pl < 4; ++pl) {
+    uint4* d = reinterpret_cast<uint4*>(a8.at(p, 2 * b, kg, pl));  // rows 2b, 2b + 1: one 32-byte sector
+    d[0] = make_uint4(pa[pl][0], pa[pl][1], pa[pl][2], pa[pl][3]);
+    d[1] = make_uint4(pb[pl][0], pb[pl][1], pb[pl][2], pb[pl][3]);
   }
 }
 
