@@ -409,6 +409,7 @@ struct StageProf {
     }
     n = 0;
     on = false;
+    cudaGetLastError();
   }
 };
 static thread_local StageProf g_sprof;
@@ -1322,6 +1323,7 @@ struct Engine {
     st->ms_coltor = (float)ph[5];
     c->plog.clear();
     c->evp_used = 0;
+    cudaGetLastError();  // an interval that could not be timed must not surface as a later launch error
   }
 
   static int check_keys(gpir_ctx* c, const int32_t* slots, int B, uint32_t stages, bool need_rgsw) {
@@ -1931,6 +1933,7 @@ int gpir_ctx_device(const gpir_ctx* c) { return c ? c->device : -1; }
 int gpir_set_graphs(gpir_ctx* c, int on) {
   if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   c->use_graph = on ? 1 : 0;
   return 0;
 }
@@ -1938,6 +1941,7 @@ int gpir_set_graphs(gpir_ctx* c, int on) {
 int gpir_set_capacity(gpir_ctx* c, uint64_t sel_budget_bytes, uint32_t max_batch) {
   if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   c->sel_budget = (size_t)sel_budget_bytes;
   c->max_batch = (int)max_batch;
   return 0;
@@ -1946,6 +1950,7 @@ int gpir_set_capacity(gpir_ctx* c, uint64_t sel_budget_bytes, uint32_t max_batch
 int gpir_set_rowsel_engine(gpir_ctx* c, int engine) {
   if (!c || engine < 0 || engine > 2) FAIL(GPIR_INVALID_ARGUMENT, "engine must be 0 (auto), 1 (CUDA cores) or 2 (tensor cores)");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   c->rowsel_engine = engine;
   return 0;
 }
@@ -1961,6 +1966,7 @@ static gpir_db* db_encode_impl(gpir_ctx* c, const uint8_t* records, bool on_devi
     return nullptr;
   }
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   cudaSetDevice(c->device);
   gpir_db* db = new gpir_db();
   db->d0 = d0;
@@ -2009,6 +2015,7 @@ gpir_db* gpir_db_upload(gpir_ctx* c, const uint32_t* pmajor, uint32_t d0, uint32
     return nullptr;
   }
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   cudaSetDevice(c->device);
   gpir_db* db = new gpir_db();
   db->d0 = d0;
@@ -2078,6 +2085,7 @@ gpir_db* gpir_db_load(gpir_ctx* c, const char* path, uint32_t expect_plain_bits,
   if (!d0 || !d1 || (d1 & (d1 - 1)) || layout > 1) return fail("bad database geometry", 6);
   const size_t words = (size_t)d0 * d1 * k * n;
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   cudaSetDevice(c->device);
   gpir_db* db = new gpir_db();
   db->d0 = d0;
@@ -2162,6 +2170,7 @@ int gpir_db_save(gpir_ctx* c, const gpir_db* db, const char* path, uint32_t reco
 int gpir_db_compact(gpir_ctx* c, gpir_db* db) {
   if (!c || !db) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   switch (c->logn * 10000 + c->k * 100 + c->ell) {
     case 120405: return Engine<12, 4, 5>::db_compact(c, db);
@@ -2175,6 +2184,7 @@ int gpir_db_download(gpir_ctx* c, const gpir_db* db, uint32_t* out) {
   if (!c || !db || !out) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
   if (db->compact) FAIL(GPIR_INVALID_STATE, "compact database: only the byte-plane image is resident");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   const size_t words = (size_t)db->d0 * db->d1 * c->k * c->n;
   DevBuf tmp;
@@ -2191,6 +2201,7 @@ void gpir_db_destroy(gpir_ctx* c, gpir_db* db) {
   if (!db) return;
   if (c) {
     std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     db->data.release();
@@ -2259,6 +2270,7 @@ static int install_keys_brv(gpir_ctx* c, int slot, const uint32_t* d_evks, uint3
 int gpir_keys_put(gpir_ctx* c, int slot, const uint32_t* evks, uint32_t stages, const uint32_t* sk_rgsw) {
   if (!c || slot < 0 || (stages && !evks)) FAIL(GPIR_INVALID_ARGUMENT, "invalid key upload");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   const size_t CT = c->ct_words();
   const size_t ell = c->ell;
@@ -2289,6 +2301,7 @@ int gpir_client_keygen(gpir_ctx* c, int slot, uint32_t stages, uint64_t seed, ui
                        int8_t* secret_out) {
   if (!c || slot < 0 || stages > 31) FAIL(GPIR_INVALID_ARGUMENT, "invalid client keygen request");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   c->error_bound = error_bound;
   switch (c->logn * 10000 + c->k * 100 + c->ell) {
@@ -2308,6 +2321,7 @@ int gpir_client_queries(gpir_ctx* c, const int8_t* secret, uint32_t plain_bits, 
   if (!c || !secret || !i_star || !j_star || !queries_out || !d0 || !d1 || (d1 & (d1 - 1)))
     FAIL(GPIR_INVALID_ARGUMENT, "invalid client query request");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   c->error_bound = error_bound;
   if (!count) return 0;
@@ -2321,6 +2335,7 @@ int gpir_client_queries(gpir_ctx* c, const int8_t* secret, uint32_t plain_bits, 
 int gpir_keys_drop(gpir_ctx* c, int slot) {
   if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   if (slot >= 0 && (uint32_t)slot < c->key_slots) {
     c->slot_stages[slot] = -1;
     c->slot_rgsw[slot] = 0;
@@ -2348,6 +2363,7 @@ int gpir_answer_batch_dev(gpir_ctx* c, const gpir_db* db, const uint32_t* d_quer
   if (!c || !db || !d_queries || !key_slots || !d_responses) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
   if (B == 0) return 0;
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   cudaStream_t s = pick_stream(c, stream);
   if (stats) memset(stats, 0, sizeof(*stats));
@@ -2363,6 +2379,7 @@ int gpir_answer_batch(gpir_ctx* c, const gpir_db* db, const uint32_t* queries, c
   if (!c || !db || !queries || !key_slots || !responses_out) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
   if (B == 0) return 0;
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
   const size_t words = (size_t)B * c->ct_words();
@@ -2389,6 +2406,7 @@ int gpir_answer_batch(gpir_ctx* c, const gpir_db* db, const uint32_t* queries, c
 int gpir_set_stage_timing(gpir_ctx* c, int on) {
   if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   c->stage_timing = on ? 1 : 0;
   return 0;
 }
@@ -2396,6 +2414,7 @@ int gpir_set_stage_timing(gpir_ctx* c, int on) {
 int gpir_stage_times(gpir_ctx* c, gpir_stage_time* out, uint32_t cap) {
   if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   const uint32_t m = std::min<uint32_t>(cap, (uint32_t)c->last_stages.size());
   for (uint32_t i = 0; i < m && out; ++i) out[i] = c->last_stages[i];
   return (int)c->last_stages.size();
@@ -2421,6 +2440,7 @@ int gpir_shard_answer(gpir_ctx* c, const gpir_db* db, uint32_t d1_total, const u
                       gpir_stats* stats) {
   if (!c || !db || !d_queries || !key_slots || !d_partials) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   cudaStream_t s = pick_stream(c, stream);
   if (stats) memset(stats, 0, sizeof(*stats));
@@ -2444,6 +2464,7 @@ int gpir_sharded_expand(gpir_ctx* c, uint32_t d0, uint32_t d1, const uint32_t* d
   if (!c || !d_queries || !key_slots || !d_rows || !B || !d0 || !d1 || (d1 & (d1 - 1)))
     FAIL(GPIR_INVALID_ARGUMENT, "invalid sharded expansion input");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   cudaStream_t s = pick_stream(c, stream);
   int rc;
@@ -2461,6 +2482,7 @@ int gpir_sharded_rowsel(gpir_ctx* c, const gpir_db* db, const uint32_t* d_rows, 
                         void* stream) {
   if (!c || !db || !d_rows || !d_partial || !B) FAIL(GPIR_INVALID_ARGUMENT, "invalid sharded rowsel input");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   cudaStream_t s = pick_stream(c, stream);
   int rc;
@@ -2484,6 +2506,7 @@ int gpir_sharded_rowsel(gpir_ctx* c, const gpir_db* db, const uint32_t* d_rows, 
 int gpir_sharded_rgsw(gpir_ctx* c, uint32_t bit_lo, uint32_t bit_hi, uint32_t* d_rgsw, void* stream) {
   if (!c || !d_rgsw) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   cudaStream_t s = pick_stream(c, stream);
   int rc;
@@ -2500,6 +2523,7 @@ int gpir_sharded_rgsw(gpir_ctx* c, uint32_t bit_lo, uint32_t bit_hi, uint32_t* d
 int gpir_layout_convert(gpir_ctx* c, const uint32_t* d_in, uint32_t* d_out, uint64_t polys, void* stream) {
   if (!c || !d_in || !d_out) FAIL(GPIR_INVALID_ARGUMENT, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   cudaStream_t s = pick_stream(c, stream);
   int rc = bitrev_rows(c, d_in, d_out, (size_t)polys * c->k, s);
@@ -2515,6 +2539,7 @@ int gpir_layout_convert(gpir_ctx* c, const uint32_t* d_in, uint32_t* d_out, uint
 int gpir_sharded_coltor(gpir_ctx* c, uint32_t* d_sums, uint32_t B, uint32_t* d_out, void* stream) {
   if (!c || !d_sums || !d_out || !B) FAIL(GPIR_INVALID_ARGUMENT, "invalid sharded coltor input");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   cudaStream_t s = pick_stream(c, stream);
   int rc;
@@ -2537,6 +2562,7 @@ int gpir_sharded_rowsel_coltor(gpir_ctx* c, const gpir_db* db, const uint32_t* d
   if (!c || !db || !d_rows || !d_out || !B) FAIL(GPIR_INVALID_ARGUMENT, "invalid sharded rowsel/coltor input");
   if (db->d1 > 1 && !d_rgsw_low) FAIL(GPIR_INVALID_ARGUMENT, "missing low-bit RGSW rows");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   cudaStream_t s = pick_stream(c, stream);
   int rc;
@@ -2556,6 +2582,7 @@ int gpir_coltor_dev(gpir_ctx* c, const uint32_t* d_cts, uint32_t B, uint32_t C, 
                     uint32_t* d_out, void* stream) {
   if (!c || !d_cts || !d_out || !C || (C & (C - 1))) FAIL(GPIR_INVALID_ARGUMENT, "invalid tournament input");
   std::lock_guard<std::mutex> lk(c->mu);
+  cudaGetLastError();  // a stale non-sticky error of an earlier call must not fail this one
   CK(cudaSetDevice(c->device));
   cudaStream_t s = pick_stream(c, stream);
   int rc;
@@ -2571,6 +2598,7 @@ int gpir_coltor_dev(gpir_ctx* c, const uint32_t* d_cts, uint32_t B, uint32_t C, 
 
 #define OP_DISPATCH(CALL)                                                   \
   std::lock_guard<std::mutex> lk(c->mu);                                    \
+  cudaGetLastError();                                                       \
   CK(cudaSetDevice(c->device));                                             \
   switch (c->logn * 10000 + c->k * 100 + c->ell) {                          \
     case 120405: return Engine<12, 4, 5>::CALL;                             \
