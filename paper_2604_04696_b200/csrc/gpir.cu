@@ -52,7 +52,7 @@ static thread_local std::string g_err;
   do {                                                                                   \
     cudaError_t e_ = cudaGetLastError();                                                 \
     if (e_ != cudaSuccess) {                                                             \
-      g_err = std::string("kernel launch: ") + cudaGetErrorString(e_);                   \
+      g_err = std::string("kernel launch (gpir.cu:") + std::to_string(__LINE__) + "): " + cudaGetErrorString(e_); \
       return GPIR_CUDA_ERROR;                                                            \
     }                                                                                    \
   } while (0)
@@ -413,6 +413,27 @@ struct StageProf {
   }
 };
 static thread_local StageProf g_sprof;
+
+// Dynamic shared memory attribute of a kernel, per device, only ever raised:
+// the kernels are shared by every Engine instantiation, so one global record
+// (a per-instantiation cache could lower the attribute below what another
+// instantiation's launch needs, failing it with "invalid argument").  Set
+// outside graph captures (the first, eager call of a shape).
+static int raise_smem_attr(int device, const void* kern, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::tuple<int, const void*, size_t>> smem_set;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& ks : smem_set)
+    if (std::get<0>(ks) == device && std::get<1>(ks) == kern) {
+      if (std::get<2>(ks) >= smem) return 0;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      std::get<2>(ks) = smem;
+      return 0;
+    }
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_set.emplace_back(device, kern, smem);
+  return 0;
+}
 
 template <int LOGN, int K, int ELL>
 struct Engine {
@@ -800,17 +821,7 @@ struct Engine {
     return 0;
   }
 
-  static int set_smem_attr(gpir_ctx* c, const void* kern, size_t smem) {
-    // the attribute is set once per (device, kernel, size): no API calls inside a graph capture
-    static std::mutex mu;
-    static std::vector<std::tuple<int, const void*, size_t>> smem_set;
-    std::lock_guard<std::mutex> lk(mu);
-    for (auto& ks : smem_set)
-      if (std::get<0>(ks) == c->device && std::get<1>(ks) == kern && std::get<2>(ks) >= smem) return 0;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set.emplace_back(c->device, kern, smem);
-    return 0;
-  }
+  static int set_smem_attr(gpir_ctx* c, const void* kern, size_t smem) { return raise_smem_attr(c->device, kern, smem); }
 
   // RowSel: tensor-core path (byte-plane u8 GEMMs, rowsel_tc.cuh) when the
   // shape allows, else the CUDA-core kernel.  ev_mid (if non-null) is
