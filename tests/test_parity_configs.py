@@ -109,3 +109,23 @@ def test_interleaved_coltor_all_modes(B, ct_mode):
         assert np.array_equal(out, want)
     finally:
         _release(ctx, h, slots)
+
+
+def test_graphs_with_alternating_batch_classes():
+    """Batches alternating between B = 2 (the streamed-operand RowSel, its own DB
+    byte-plane layout) and B = 40 (the TMEM-resident RowSel, another layout) with
+    CUDA graphs on: each layout change repacks the DB planes and must retire the
+    recorded graphs of the other class, so every call stays bit-exact."""
+    po = O.test_params()
+    d0, d1, B = 32, 64, 40
+    G, nat, ctx, h, db, evks, rg, qs, slots = _setup(po, d0, d1, B, seed=4040)
+    try:
+        nat.check(ctx.lib.gpir_set_graphs(ctx.h, 1), "graphs on")
+        want = O.answer_batch(qs.astype(np.uint64), evks.astype(np.uint64), rg.astype(np.uint64),
+                              db.astype(np.uint64), d0, d1, po)
+        q2, s2 = np.ascontiguousarray(qs[:2]), np.ascontiguousarray(slots[:2])
+        for _ in range(4):  # eager, record, replay, replay -- for both classes, interleaved
+            assert np.array_equal(_answer(nat, ctx, h, q2, s2), want[:2])
+            assert np.array_equal(_answer(nat, ctx, h, qs, slots), want)
+    finally:
+        _release(ctx, h, slots)
