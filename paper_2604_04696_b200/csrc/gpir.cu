@@ -1396,7 +1396,13 @@ struct Engine {
     const uint32_t total = leaves_of(d0, d1, ELL), bits = ilog2(d1);
     int rc;
     if ((rc = check_keys(c, slots, B, stages_of(total), bits > 0))) return rc;
-    if ((rc = ensure_ws(c, B, total, d1, bits))) return rc;
+    // expansion workspace only: the selection / tournament buffers are sized by the steps that use them
+    const size_t ctb = CT * 4;
+    if ((rc = c->ws_state0.ensure((size_t)B * total * ctb))) return rc;
+    if ((rc = c->ws_state1.ensure((size_t)B * total * ctb))) return rc;
+    if ((rc = c->ws_arows.ensure((size_t)B * std::max<uint32_t>(bits, 1) * ELL * ctb))) return rc;
+    if ((rc = c->ws_crows.ensure((size_t)B * std::max<uint32_t>(bits, 1) * 2 * ELL * ctb))) return rc;
+    if ((rc = c->ws_kslot.ensure((size_t)B * 4))) return rc;
     CK(cudaMemcpyAsync(c->ws_kslot.p, slots, (size_t)B * 4, cudaMemcpyHostToDevice, s));
     if ((rc = bitrev_rows(c, d_q, c->ws_state0.as<u32>(), (size_t)B * 2 * K, s))) return rc;
     uint32_t launches = 0;
@@ -1445,6 +1451,11 @@ struct Engine {
     if (!c->sh_leaves || (uint32_t)B != c->sh_B) FAIL(GPIR_INVALID_STATE, "gpir_sharded_expand must precede gpir_sharded_coltor");
     const uint32_t d1 = c->sh_d1, bits = ilog2(d1), total = c->sh_total, d0 = c->sh_d0;
     const size_t rows = (size_t)B * d1 * 2 * K;
+    int rc0;
+    if ((rc0 = c->ws_ct0.ensure(std::max(c->ws_ct0.bytes, (size_t)B * std::max<uint32_t>(d1 / 2, 1) * CT * 4))))
+      return rc0;
+    if ((rc0 = c->ws_ct1.ensure(std::max(c->ws_ct1.bytes, (size_t)B * std::max<uint32_t>(d1 / 4, 1) * CT * 4))))
+      return rc0;
     k_mod_rows<<<(unsigned)((rows * N + 255) / 256), 256, 0, s>>>(d_sums, rows, LOGN, K, c->tb);
     CKL();
     u32* cur = d_sums;
