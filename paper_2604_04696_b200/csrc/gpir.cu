@@ -585,9 +585,8 @@ struct Engine {
         const int nn = (int)std::min(cn, cts - m0);
         k_xp_dcp<LOGN, K, ELL><<<nn, T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_dig.as<int>(), c->tb, c->cc, c->tc);
         CKL();
-        k_xp_nttmac<LOGN, K, ELL><<<nn * K, T, 0, s>>>(in, in_b, M, (int)m0, pairs,
-                                                                         c->ws_dig.as<int>(), rows, out, out_b,
-                                                                         c->tb, c->tc);
+        launch_xp_nttmac<LOGN, K, ELL>(nn * K, s, in, in_b, M, (int)m0, pairs, c->ws_dig.as<int>(), rows, out, out_b,
+                                       c->tb, c->tc);
         CKL();
         *launches += 2;
       }
@@ -610,8 +609,8 @@ struct Engine {
                                                                           c->ws_dig.as<int>(), c->tb, c->cc, ELL - 1);
       CKL();
       if (mode == 3) {
-        k_xp_nttmac<LOGN, K, ELL><<<nn * K, T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_dig.as<int>(), rows, out,
-                                                       out_b, c->tb, c->tc);
+        launch_xp_nttmac<LOGN, K, ELL>(nn * K, s, in, in_b, M, (int)m0, pairs, c->ws_dig.as<int>(), rows, out, out_b,
+                                       c->tb, c->tc);
         CKL();
         *launches += 3;
         continue;

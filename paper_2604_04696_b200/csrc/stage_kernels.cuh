@@ -245,11 +245,14 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, K2_MINB)
   }
 }
 
-// K2, external product / ColTor: ct (m0 + blockIdx.x / K), output limb blockIdx.x % K
-template <int LOGN, int K, int ELL>
+// K2, external product / ColTor: ct (m0 + blockIdx.x / K), output limb blockIdx.x % K.
+// PAIRS (0: plain cts, 1: ColTor pairs, 2: pair-interleaved) is a template
+// parameter: with it known the kernel fits 80 registers without spills.
+template <int LOGN, int K, int ELL, int PAIRS>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T, K2_MINB)
-    k_xp_nttmac(const u32* __restrict__ in, size_t in_b, int M_per_b, int m0, int pairs, const int* __restrict__ dig,
-                RowsDesc rows, u32* __restrict__ out, size_t out_b, Tables tb, const __grid_constant__ TwConst tc) {
+    k_xp_nttmac_t(const u32* __restrict__ in, size_t in_b, int M_per_b, int m0, const int* __restrict__ dig,
+                  RowsDesc rows, u32* __restrict__ out, size_t out_b, Tables tb, const __grid_constant__ TwConst tc) {
+  constexpr int pairs = PAIRS;
   constexpr int N = 1 << LOGN;
   __shared__ __align__(16) u32 xbuf[NttCfg<LOGN>::XBUF_WORDS];
   NttState ns{xbuf, 0};
@@ -301,6 +304,21 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, K2_MINB)
     reinterpret_cast<uint4*>(d + (size_t)i * N + i0)[h] = make_uint4(sa[0], sa[1], sa[2], sa[3]);
     reinterpret_cast<uint4*>(d + (size_t)(K + i) * N + i0)[h] = make_uint4(sb[0], sb[1], sb[2], sb[3]);
   }
+}
+
+// runtime `pairs` front end of k_xp_nttmac_t
+template <int LOGN, int K, int ELL>
+inline cudaError_t launch_xp_nttmac(int grid, cudaStream_t s, const u32* in, size_t in_b, int M_per_b, int m0,
+                                    int pairs, const int* dig, RowsDesc rows, u32* out, size_t out_b, const Tables& tb,
+                                    const TwConst& tc) {
+  constexpr int T = NttCfg<LOGN>::T;
+  if (pairs == 0)
+    k_xp_nttmac_t<LOGN, K, ELL, 0><<<grid, T, 0, s>>>(in, in_b, M_per_b, m0, dig, rows, out, out_b, tb, tc);
+  else if (pairs == 1)
+    k_xp_nttmac_t<LOGN, K, ELL, 1><<<grid, T, 0, s>>>(in, in_b, M_per_b, m0, dig, rows, out, out_b, tb, tc);
+  else
+    k_xp_nttmac_t<LOGN, K, ELL, 2><<<grid, T, 0, s>>>(in, in_b, M_per_b, m0, dig, rows, out, out_b, tb, tc);
+  return cudaGetLastError();
 }
 
 }  // namespace gpir
