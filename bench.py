@@ -630,6 +630,7 @@ def run_sharded(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = int(nat.load().gpir_launch_count())
     with ClockSampler(dev) as clk:
         e0.record()
         for _ in range(args.steps):
@@ -637,6 +638,7 @@ def run_sharded(args, rank, world, local_rank):
         e1.record()
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    launches = int(nat.load().gpir_launch_count()) - n0  # this rank's libgpir kernels (no graphs here)
     # e2e: this rank's queries from pinned host memory, responses back to the host
     h_q = torch.from_numpy(queries.view(np.int32)).pin_memory()
     h_o = torch.empty((b_own, queries.shape[1] * queries.shape[2] * queries.shape[3]), dtype=torch.int32).pin_memory()
@@ -679,7 +681,7 @@ def run_sharded(args, rank, world, local_rank):
                        else "uniform-random key/query material"),
             "config": common_config(args, world),
             "run": {"per_gpu_batch_owned": b_own, "compact_db": compact},
-            "gpu_launches": None,
+            "gpu_launches": launches,
             "e2e": {"value": B / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": queries.nbytes * world,
                     "d2h_bytes_per_step": queries.nbytes * world},
             "comm_bytes_per_step": {"measured": {"after_expand": float(stats[2]), "after_coltor": float(stats[3]),

@@ -101,6 +101,9 @@ int gpir_set_rowsel_engine(gpir_ctx* ctx, int engine);
  * second call and replay the graph from the third; any device (re)allocation
  * invalidates the recorded graphs. */
 int gpir_set_graphs(gpir_ctx* ctx, int on);
+/* Kernels this library has launched eagerly so far, process-wide (launches inside
+ * replayed CUDA graphs are not counted). */
+uint64_t gpir_launch_count(void);
 /* Capacity path knobs (0 = automatic): the bytes the (B, d1) RowSel selection
  * may occupy before RowSel and the low ColTor stages run per power-of-two
  * column window (default 16 GiB), and the largest sub-batch served at once

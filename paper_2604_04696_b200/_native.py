@@ -45,6 +45,7 @@ _SIGS = {
     "gpir_set_rowsel_engine": (C.c_int, [C.c_void_p, C.c_int]),
     "gpir_set_graphs": (C.c_int, [C.c_void_p, C.c_int]),
     "gpir_set_capacity": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32]),
+    "gpir_launch_count": (C.c_uint64, []),
     "gpir_db_encode": (C.c_void_p, [C.c_void_p, _u8p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
     "gpir_db_upload": (C.c_void_p, [C.c_void_p, _u32p, C.c_uint32, C.c_uint32]),
     "gpir_db_encode_dev": (C.c_void_p, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),

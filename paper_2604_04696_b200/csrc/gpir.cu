@@ -48,8 +48,12 @@ static thread_local std::string g_err;
     }                                                                                   \
   } while (0)
 
+// kernels launched eagerly by this library (graph replays not included): gpir_launch_count
+static std::atomic<uint64_t> g_launches{0};
+
 #define CKL()                                                                            \
   do {                                                                                   \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                                  \
     cudaError_t e_ = cudaGetLastError();                                                 \
     if (e_ != cudaSuccess) {                                                             \
       g_err = std::string("kernel launch (gpir.cu:") + std::to_string(__LINE__) + "): " + cudaGetErrorString(e_); \
@@ -1950,6 +1954,8 @@ void gpir_ctx_destroy(gpir_ctx* c) {
 }
 
 int gpir_ctx_device(const gpir_ctx* c) { return c ? c->device : -1; }
+
+uint64_t gpir_launch_count(void) { return g_launches.load(); }
 
 int gpir_set_graphs(gpir_ctx* c, int on) {
   if (!c) FAIL(GPIR_INVALID_ARGUMENT, "null context");
