@@ -873,7 +873,9 @@ struct Engine {
       ta.KN = KN;
       ta.logn = LOGN;
       ta.KC = r.KC;
-      ta.units = KN * r.mtiles;
+      static const int pair_env = getenv("GPIR_TK_PAIR") ? atoi(getenv("GPIR_TK_PAIR")) : 0;
+      ta.pair = (pair_env && r.mtiles % 2 == 0) ? 1 : 0;
+      ta.units = KN * (ta.pair ? r.mtiles / 2 : r.mtiles);
       const size_t slot = (size_t)128 * r.KC;
       const size_t fixed = (2 * TK_MAX_SLOTS + 16) * 8 + 16;
       ta.slots = std::min<int>(TK_MAX_SLOTS, (int)((226u * 1024u - fixed) / slot));
@@ -888,7 +890,23 @@ struct Engine {
         CK(cudaMemsetAsync(tprof.p, 0, tprof.bytes, s));
         ta.prof = tprof.as<unsigned long long>();
       }
-      k_rowsel_tk<<<grid, TK_THREADS, smem, s>>>(ta, c->tb);
+      if (ta.pair) {  // clusters of 2 CTAs: the two row tiles of each p share the DB tiles by multicast
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * std::min(ta.units, c->num_sms / 2));
+        cfg.blockDim = dim3(TK_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, k_rowsel_tk, ta, c->tb));
+      } else {
+        k_rowsel_tk<<<grid, TK_THREADS, smem, s>>>(ta, c->tb);
+      }
       CKL();
       if (tprof_on) {
         std::vector<unsigned long long> h((size_t)grid * 8);
@@ -897,8 +915,8 @@ struct Engine {
         double sum[8] = {0};
         for (int g = 0; g < grid; ++g)
           for (int k = 0; k < 8; ++k) sum[k] += (double)h[(size_t)g * 8 + k] / grid;
-        fprintf(stderr, "[tk prof] avg cycles/CTA: mma_wait_drain+A %.0f mma_wait_data %.0f mma_issue_B %.0f epi_wait %.0f epi_work %.0f\n",
-                sum[0], sum[1], sum[2], sum[3], sum[4]);
+        fprintf(stderr, "[tk prof] avg cycles/CTA: mma_wait_drain+A %.0f mma_wait_data %.0f mma_issue_B %.0f epi_wait %.0f epi_work %.0f (data wait at unit starts %.0f, inside units %.0f)\n",
+                sum[0], sum[1], sum[2], sum[3], sum[4], sum[5], sum[6]);
         tprof.release();
       }
       // the standard ciphertext layout: ColTor's first stage reads it faster than the pair-interleaved
@@ -966,8 +984,8 @@ struct Engine {
         double sum[8] = {0};
         for (int g = 0; g < grid; ++g)
           for (int k = 0; k < 8; ++k) sum[k] += (double)h[(size_t)g * 8 + k] / grid;
-        fprintf(stderr, "[tc prof] avg cycles/CTA: mma_wait_tmem %.0f mma_wait_data %.0f mma_issue %.0f epi_wait %.0f epi_work %.0f\n",
-                sum[0], sum[1], sum[2], sum[3], sum[4]);
+        fprintf(stderr, "[tc prof] avg cycles/CTA: mma_wait_tmem %.0f mma_wait_data %.0f mma_issue %.0f epi_wait %.0f epi_work %.0f (data wait at unit starts %.0f, inside units %.0f)\n",
+                sum[0], sum[1], sum[2], sum[3], sum[4], sum[5], sum[6]);
         profbuf.release();
       }
       ++*launches;

@@ -74,6 +74,13 @@ __device__ __forceinline__ void umma_i8_ta(uint32_t tmem_d, uint32_t tmem_a, uin
 __device__ __forceinline__ void tmem_cp_128x256b(uint32_t tmem_dst, uint64_t sdesc) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tmem_dst), "l"(sdesc));
 }
+// commit arriving on the mbarrier at the same offset in every CTA of ctamask
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t ctamask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(ctamask)
+               : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -591,6 +598,7 @@ struct TkArgs {
   int KC;       // padded K bytes per plane (multiple of 32, <= 256)
   int units;    // KN * mtiles
   int slots;    // ring depth
+  int pair;     // launched as clusters of 2 CTAs (row tiles 2j, 2j + 1 of one p): DB tiles multicast to both
   unsigned long long* prof;  // optional per-CTA cycle counters [grid][8] (GPIR_TC_PROF)
 };
 
@@ -608,10 +616,20 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
   uint64_t* dfull = empty + TK_MAX_SLOTS;  // [group]
   uint64_t* dempty = dfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
+  // pair mode (a.pair): the cluster's two CTAs take row tiles 2j and 2j + 1 of the
+  // same p, so every DB tile is needed by both: CTA r loads the tiles with
+  // (tile index % 2 == r) and multicasts them to both; a ring slot is refilled
+  // only after both CTAs' MMAs have released it (their commits multicast to
+  // both empty barriers: count 2).  Halves the DB bytes each SM pulls from L2
+  // and the bulk copies it issues.
+  const uint32_t crank = a.pair ? cluster_ctarank() : 0u;
+  const int ustart = a.pair ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int ustep = a.pair ? (int)cluster_count_x() : (int)gridDim.x;
+  const int mtiles_u = a.pair ? a.mtiles / 2 : a.mtiles;  // row-tile units per p
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], a.pair ? 2 : 1);
     }
     for (int g = 0; g < 2; ++g) {
       mbar_init(&dfull[g], 1);
@@ -626,6 +644,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
   }
   tc_fence_before();
   __syncthreads();
+  if (a.pair) cluster_sync_all();  // both CTAs' barriers exist before any multicast reaches them
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   const int kst = a.KC >> 5;  // MMA K steps (32 bytes each)
@@ -633,8 +652,8 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
   if (warp == 0) {  // producer: per unit the 4 A planes, then the unit's DB tiles
     const uint64_t pol_once = l2_policy_evict_first();
     uint32_t item = 0;
-    for (int un = blockIdx.x; un < a.units; un += gridDim.x) {
-      const int p = un / a.mtiles, mt = un % a.mtiles;
+    for (int un = ustart; un < a.units; un += ustep) {
+      const int p = un / mtiles_u, mt = a.pair ? 2 * (un % mtiles_u) + (int)crank : un % mtiles_u;
       // (L2 prefetches of the next unit's A planes and of DB tiles ahead of the ring were
       // measured: no faster, +24% DRAM reads)
       for (int it = 0; it < 4 + a.ntiles; ++it, ++item) {
@@ -646,8 +665,11 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
           if (it < 4)
             bulk_g2s_hint(dst, a.A8 + ((size_t)(p * a.mtiles + mt) * 4 + it) * slot_bytes, slot_bytes, &full[s],
                           pol_once);
-          else
+          else if (!a.pair)
             bulk_g2s(dst, a.D8 + ((size_t)p * a.ntiles_db + a.nt0 + (it - 4)) * slot_bytes, slot_bytes, &full[s]);
+          else if ((uint32_t)((it - 4) & 1) == crank)
+            bulk_g2s_mc(dst, a.D8 + ((size_t)p * a.ntiles_db + a.nt0 + (it - 4)) * slot_bytes, slot_bytes, &full[s],
+                        (uint16_t)3);
         }
         __syncwarp();
       }
@@ -657,7 +679,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
       uint32_t item = 0, tile = 0;
       const uint32_t acol = (uint32_t)a.KC >> 2;  // TMEM columns per A plane
       const uint32_t acc0 = tbase + TK_ACC0;
-      for (int un = blockIdx.x; un < a.units; un += gridDim.x) {
+      for (int un = ustart; un < a.units; un += ustep) {
         const uint32_t item_a = item;  // the unit's A planes: ring items item_a .. item_a + 3
         item += 4;
         for (int nt = 0; nt < a.ntiles; ++nt, ++item, ++tile) {
@@ -674,7 +696,10 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
               const uint32_t abase = smem_u32(tk_smem + (size_t)sa * slot_bytes);
               for (int ks = 0; ks < kst; ++ks)
                 tmem_cp_128x256b(tbase + sp * acol + 8 * ks, umma_desc(abase + ks * 4096, 2048, 128));
-              umma_commit(&empty[sa]);  // slot free once the copies have landed
+              if (a.pair)  // slot free once the copies have landed (both CTAs count both releases)
+                umma_commit_mc(&empty[sa], (uint16_t)3);
+              else
+                umma_commit(&empty[sa]);
             }
           }
           mbar_wait(&full[sb], phb);
@@ -718,10 +743,14 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
             tk_mma(acc0 + 192, ak + 2 * acol, bk + 1 * bpl, 1u);
           }
           umma_commit(&dfull[1]);
-          umma_commit(&empty[sb]);  // DB tile free once both groups have read it
+          if (a.pair)  // DB tile free once both groups of both CTAs have read it
+            umma_commit_mc(&empty[sb], (uint16_t)3);
+          else
+            umma_commit(&empty[sb]);
           if (a.prof) {
             long long t4 = clock64();
             a.prof[blockIdx.x * 8 + 1] += t1 - t0;            // waits for data (and the A copies)
+            a.prof[blockIdx.x * 8 + (nt == 0 ? 5 : 6)] += t1 - t0;  // ... at unit starts / inside units
             a.prof[blockIdx.x * 8 + 0] += (t2 - t1) + (t3 - t2 - 0);  // waits for drains + group A issue
             a.prof[blockIdx.x * 8 + 2] += t4 - t3;            // group B issue
           }
@@ -735,8 +764,8 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
     const uint32_t lb = tbase + ((uint32_t)(quad * 32) << 16) + TK_ACC0 + 8 * cq;
     const bool vec = (a.d1 & 3) == 0;
     uint32_t tile = 0;
-    for (int un = blockIdx.x; un < a.units; un += gridDim.x) {
-      const int p = un / a.mtiles, mt = un % a.mtiles;
+    for (int un = ustart; un < a.units; un += ustep) {
+      const int p = un / mtiles_u, mt = a.pair ? 2 * (un % mtiles_u) + (int)crank : un % mtiles_u;
       const Modulus M = tb.mod[p >> a.logn];
       const int m = mt * 128 + quad * 32 + lane;
       const bool act = m < a.M;
@@ -801,6 +830,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
     }
   }
   __syncthreads();
+  if (a.pair) cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
