@@ -875,6 +875,8 @@ struct Engine {
       ta.KC = r.KC;
       static const int pair_env = getenv("GPIR_TK_PAIR") ? atoi(getenv("GPIR_TK_PAIR")) : 0;
       ta.pair = (pair_env && r.mtiles % 2 == 0) ? 1 : 0;
+      static const int aring_env = getenv("GPIR_TK_ARING") ? atoi(getenv("GPIR_TK_ARING")) : 0;
+      ta.aring = (aring_env && !ta.pair) ? 1 : 0;
       ta.units = KN * (ta.pair ? r.mtiles / 2 : r.mtiles);
       const size_t slot = (size_t)128 * r.KC;
       const size_t fixed = (2 * TK_MAX_SLOTS + 16) * 8 + 16;

@@ -583,7 +583,7 @@ constexpr int TK_NT = 32;
 constexpr int TK_ACC0 = 256;  // first accumulator column
 constexpr int TK_MAX_SLOTS = 8;
 constexpr int TK_EPI_WARPS = 16;
-constexpr int TK_THREADS = 64 + 32 * TK_EPI_WARPS;
+constexpr int TK_THREADS = 96 + 32 * TK_EPI_WARPS;  // producer, MMA, 16 epilogue warps, A producer (aring mode)
 
 struct TkArgs {
   const uint8_t* A8;
@@ -599,6 +599,7 @@ struct TkArgs {
   int units;    // KN * mtiles
   int slots;    // ring depth
   int pair;     // launched as clusters of 2 CTAs (row tiles 2j, 2j + 1 of one p): DB tiles multicast to both
+  int aring;    // ring slots 0..3 hold the A planes only (the next unit's A streams in a whole unit ahead), the rest the DB tiles
   unsigned long long* prof;  // optional per-CTA cycle counters [grid][8] (GPIR_TC_PROF)
 };
 
@@ -649,7 +650,39 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
   const uint32_t tbase = *tmem_slot;
   const int kst = a.KC >> 5;  // MMA K steps (32 bytes each)
 
-  if (warp == 0) {  // producer: per unit the 4 A planes, then the unit's DB tiles
+  if (a.aring && (warp == 0 || warp == TK_THREADS / 32 - 1)) {
+    // dedicated A slots: warp 0 streams the DB tiles through slots 4.., the last warp
+    // the A planes through slots 0..3 (plane sp of a unit reuses the slot of plane sp of
+    // the previous one, released right after that unit's tcgen05.cp)
+    const uint64_t pol_once = l2_policy_evict_first();
+    const int NSD = NS - 4;
+    uint32_t k = 0, d = 0;
+    for (int un = ustart; un < a.units; un += ustep, ++k) {
+      const int p = un / mtiles_u, mt = un % mtiles_u;
+      if (warp != 0) {
+        for (int sp = 0; sp < 4; ++sp) {
+          mbar_wait(&empty[sp], (k & 1) ^ 1);
+          if (elect_one()) {
+            mbar_expect_tx(&full[sp], slot_bytes);
+            bulk_g2s_hint(tk_smem + (size_t)sp * slot_bytes, a.A8 + ((size_t)(p * a.mtiles + mt) * 4 + sp) * slot_bytes,
+                          slot_bytes, &full[sp], pol_once);
+          }
+          __syncwarp();
+        }
+      } else {
+        for (int nt = 0; nt < a.ntiles; ++nt, ++d) {
+          const uint32_t s = 4 + d % NSD, ph = (d / NSD) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (elect_one()) {
+            mbar_expect_tx(&full[s], slot_bytes);
+            bulk_g2s(tk_smem + (size_t)s * slot_bytes, a.D8 + ((size_t)p * a.ntiles_db + a.nt0 + nt) * slot_bytes,
+                     slot_bytes, &full[s]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp == 0) {  // producer: per unit the 4 A planes, then the unit's DB tiles
     const uint64_t pol_once = l2_policy_evict_first();
     uint32_t item = 0;
     for (int un = ustart; un < a.units; un += ustep) {
@@ -679,19 +712,21 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
       uint32_t item = 0, tile = 0;
       const uint32_t acol = (uint32_t)a.KC >> 2;  // TMEM columns per A plane
       const uint32_t acc0 = tbase + TK_ACC0;
-      for (int un = ustart; un < a.units; un += ustep) {
+      uint32_t k = 0, d = 0;
+      for (int un = ustart; un < a.units; un += ustep, ++k) {
         const uint32_t item_a = item;  // the unit's A planes: ring items item_a .. item_a + 3
-        item += 4;
-        for (int nt = 0; nt < a.ntiles; ++nt, ++item, ++tile) {
-          const uint32_t sb = item % NS, phb = (item / NS) & 1;
+        if (!a.aring) item += 4;
+        for (int nt = 0; nt < a.ntiles; ++nt, ++item, ++tile, ++d) {
+          const uint32_t sb = a.aring ? 4 + d % (NS - 4) : item % NS;
+          const uint32_t phb = a.aring ? (d / (NS - 4)) & 1 : (item / NS) & 1;
           const uint64_t b0 = umma_desc(smem_u32(tk_smem + (size_t)sb * slot_bytes), 512, 128);
           const uint32_t bpl = (uint32_t)(32 * a.KC) >> 4;  // descriptor step of one B plane
           const uint32_t tph = (tile & 1) ^ 1;
           long long t0 = clock64();
           if (nt == 0) {  // the unit's four A planes into TMEM columns [sp * acol, (sp + 1) * acol)
             for (int sp = 0; sp < 4; ++sp) {
-              const uint32_t ia = item_a + sp, sa = ia % NS;
-              mbar_wait(&full[sa], (ia / NS) & 1);
+              const uint32_t ia = item_a + sp, sa = a.aring ? (uint32_t)sp : ia % NS;
+              mbar_wait(&full[sa], a.aring ? (k & 1) : (ia / NS) & 1);
               tc_fence_after();
               const uint32_t abase = smem_u32(tk_smem + (size_t)sa * slot_bytes);
               for (int ks = 0; ks < kst; ++ks)
@@ -758,7 +793,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_rowsel_tk(TkArgs a, Tables tb
       }
     }
     __syncwarp();
-  } else {  // epilogue warps 2..17: TMEM lanes 32 * (warp % 4) .., columns 8 * cq ..
+  } else if (warp < 2 + TK_EPI_WARPS) {  // epilogue warps 2..17: TMEM lanes 32 * (warp % 4) .., columns 8 * cq ..
     const int quad = warp & 3;
     const int cq = (warp - 2) >> 2;
     const uint32_t lb = tbase + ((uint32_t)(quad * 32) << 16) + TK_ACC0 + 8 * cq;
