@@ -608,14 +608,17 @@ struct Engine {
       const int nn = (int)std::min(cn, cts - m0);
       k_op_xp_intt<LOGN, K><<<dim3(2 * nn, K), T, 0, s>>>(in, in_b, M, (int)m0, pairs, c->ws_coeff.as<u32>(), c->tb, c->tc);
       CKL();
+      if (g_sprof.fine) g_sprof.mark(s, "  xp_intt");
       const size_t tot = (size_t)2 * nn * N;
       k_op_dcp<LOGN, K, ELL><<<(unsigned)((tot / 4 + 255) / 256), 256, 0, s>>>(c->ws_coeff.as<u32>(), 2 * nn,
                                                                           c->ws_dig.as<int>(), c->tb, c->cc, ELL - 1);
       CKL();
+      if (g_sprof.fine) g_sprof.mark(s, "  xp_dcp");
       if (mode == 3) {
         launch_xp_nttmac<LOGN, K, ELL>(nn * K, s, in, in_b, M, (int)m0, pairs, c->ws_dig.as<int>(), rows, out, out_b,
                                        c->tb, c->tc);
         CKL();
+        if (g_sprof.fine) g_sprof.mark(s, "  xp_nttmac");
         *launches += 3;
         continue;
       }
