@@ -94,6 +94,25 @@ def test_config_responses_bitexact(d0, d1, B):
         _release(ctx, h, slots)
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("B", [1, 33], ids=["B1", "B33"])
+def test_config3_geometry_other_batches(B):
+    """The config-3 DB (256 x 512) at a single query (the streamed-operand RowSel, M = 2)
+    and at B = 33 (2B = 66: the TMEM-resident RowSel with a nearly empty row tile), the
+    built-in plan: sampled responses equal the oracle's bit for bit."""
+    po = O.default_params(plain_bits=16)
+    d0, d1 = 256, 512
+    G, nat, ctx, h, db, evks, rg, qs, slots = _setup(po, d0, d1, B, seed=300 + B)
+    try:
+        out = _answer(nat, ctx, h, qs, slots)
+        for b in sorted({0, B - 1}):
+            want = O.answer_batch(qs[b:b + 1].astype(np.uint64), evks[b:b + 1].astype(np.uint64),
+                                  rg[b:b + 1].astype(np.uint64), db, d0, d1, po)
+            assert np.array_equal(out[b], want[0]), f"query {b}: response differs from the oracle"
+    finally:
+        _release(ctx, h, slots)
+
+
 @pytest.mark.parametrize("B", [40, 48])
 @pytest.mark.parametrize("ct_mode", [0, 1, 2, 3], ids=["op", "fused", "split", "hybrid"])
 def test_interleaved_coltor_all_modes(B, ct_mode):
