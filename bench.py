@@ -160,12 +160,18 @@ def _profile(cfg_id):
 
 
 def ncu_traffic(cfg_id, prefix):
+    """DRAM read + write bytes of the kernel over one bench step of this config: the sum over
+    its launches in the committed ncu launch list (several launches when the capacity path runs
+    RowSel per column window), else the full capture of its first launch."""
     js, name = _profile(cfg_id)
     if not js:
         return None
+    for k, d in (js.get("launch_list") or {}).items():
+        if k.startswith(prefix):
+            return d["dram_read"] + d["dram_write"], name, f"{k}, {d['launches']} launch(es), launch list"
     for k, d in js.get("kernels", {}).items():
         if k.startswith(prefix) and "traffic_bytes" in d:
-            return d["traffic_bytes"], name, k
+            return d["traffic_bytes"], name, f"{k}, --set full"
     return None
 
 
@@ -248,7 +254,7 @@ def rowsel_roofline(d0, d1, B, kn, ms, hbm, peak_kind, cfg_id):
              "peak_kind": peak_kind}
     r.update({"kernel": f"{kname} (RowSel GEMM, tcgen05.mma kind::i8 byte planes)", "frac": r["achieved"] / r["peak"],
               "traffic": tr[0] if tr else None,
-              "traffic_src": f"profiles/{tr[1]} ({tr[2]}, ncu --set full)" if tr else None,
+              "traffic_src": f"profiles/{tr[1]} ({tr[2]})" if tr else None,
               "algorithmic_bytes": rs_bytes, "avg_launch_ms": ms,
               "floors_ms": {"hbm": t_hbm * 1e3, "tensor": t_tc * 1e3}})
     return r

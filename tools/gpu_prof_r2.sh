@@ -10,7 +10,7 @@ NCU="ncu --clock-control none --profile-from-start off"
 for cfg in ${CFGS:-3 2}; do
   timeout 900 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv \
     --log-file $W/c${cfg}_launches.csv $P --config $cfg > $W/c${cfg}_list.log 2>&1
-  if [ $cfg = 2 ]; then
+  if [ $cfg = 2 ] || [ $cfg = 1 ]; then
     KS="k_rowsel_tc:0 k_op_digit_ntt:8 k_op_eq_mac_nb4:8 k_xp_nttmac:1 k_op_eq_intt:8 k_pack_planes2:0"
   else
     KS="k_rowsel_tk:0 k_y_to_cts:0 k_xp_nttmac:1 k_op_xp_intt:1 k_op_dcp:10 k_op_digit_ntt:8 k_op_eq_mac_nb4:8 k_op_eq_intt:8 k_pack_planes2:0"
